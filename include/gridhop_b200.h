@@ -1,0 +1,175 @@
+/*
+ * gridhop_b200.h — C ABI of the B200-native grid-hopping hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or CUDA
+ * types, no exceptions across the ABI. Every call returns an int status and
+ * leaves a thread-local message readable through gh_last_error(). Status
+ * codes map 1:1 onto the exception types of the reference library
+ * (/root/reference/proj/core), so the C++ wrappers in gridhop_b200.hpp can
+ * rethrow exactly what the reference throws:
+ *
+ *   GH_OK        0   success
+ *   GH_EINVAL    1   std::invalid_argument   (bad sizes / arguments)
+ *   GH_ERUNTIME  2   std::runtime_error      (stale table, window errors)
+ *   GH_EDOMAIN   3   std::domain_error       (degenerate geometry)
+ *   GH_ECUDA     4   std::runtime_error      (CUDA / device failure)
+ *
+ * Suffix `_d`: every array argument is a DEVICE pointer on the context's
+ * device (e.g. torch.Tensor.data_ptr()). No suffix: HOST pointers; the call
+ * does its own host<->device copies on the context stream and returns when
+ * the results are in host memory.
+ *
+ * Which reference interface each entry point replaces is given beside it
+ * (file:line under /root/reference/proj/core). The reference binds none of
+ * these today (it has no FFI); INTEGRATION.md shows the C++ wrapper and
+ * ctypes bindings a maintainer would add.
+ */
+#ifndef GRIDHOP_B200_H
+#define GRIDHOP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GH_ABI_VERSION 1
+
+enum gh_status { GH_OK = 0, GH_EINVAL = 1, GH_ERUNTIME = 2, GH_EDOMAIN = 3, GH_ECUDA = 4 };
+
+/* InterpScheme (include/gridhop/interp.hpp:16) + the polar scheme. */
+enum gh_scheme { GH_NEAREST = 1, GH_LINEAR = 2, GH_POLY3 = 3, GH_POLAR = 4 };
+
+/* Non-coherent combine over pairs: power sum |.|^2 (the reference,
+ * src/hopping.cpp:99) or magnitude sum |.| (BASELINE c1 wording). */
+enum gh_combine { GH_POWER = 0, GH_MAGNITUDE = 1 };
+
+/* Waveform + TX/RX pair list. Generalises WaveformConfig + SceneGeometry
+ * (include/gridhop/model.hpp:21-50) to P (tx, rx) pairs in 3-D. */
+typedef struct {
+  int32_t n_samples;   /* N fast-time samples per pair                    */
+  int32_t os_range;    /* zero-padding factor; M = os_range * N           */
+  double range_scale;  /* B / c: fast-time bins per metre of summed path  */
+  int32_t n_pairs;     /* P                                               */
+  const double* tx;    /* host [P][3] TX positions, metres                */
+  const double* rx;    /* host [P][3] RX positions, metres                */
+} gh_wave;
+
+/* LocationGrid (include/gridhop/model.hpp:77-92) in 3-D, x fastest. */
+typedef struct {
+  double origin[3];
+  double spacing[3];
+  int32_t n[3];
+} gh_grid;
+
+/* Monte-Carlo scene model: sample_scene (src/montecarlo.cpp:48-66) with the
+ * BASELINE extensions (K targets, per-pair amplitude / SNR). */
+typedef struct {
+  uint64_t seed;
+  int32_t n_targets;
+  int32_t dims;            /* 2 or 3 position draws per target            */
+  double area_lo[3];
+  double area_hi[3];
+  int32_t amp_mode;        /* 0 unit-phase shared, 1 unit-phase per pair,
+                              2 CN(0,1) shared, 3 CN(0,1) per pair         */
+  int32_t snr_mode;        /* 0 fixed, 1 U[snr_lo, snr_hi] per pair,
+                              2 noiseless                                  */
+  double snr_db;
+  double snr_lo;
+  double snr_hi;
+} gh_campaign;
+
+typedef struct gh_ctx gh_ctx;      /* one device + one stream + scratch    */
+typedef struct gh_table gh_table;  /* device-resident mapping operator     */
+
+/* ---- library / context ------------------------------------------------ */
+const char* gh_last_error(void);
+int gh_abi_version(void);
+int gh_ctx_create(int32_t device, gh_ctx** out);
+int gh_ctx_destroy(gh_ctx* ctx);
+/* The stream every call of this context is enqueued on (cudaStream_t). */
+int gh_ctx_get_stream(gh_ctx* ctx, void** stream);
+/* Use a caller-owned stream instead (e.g. torch.cuda.current_stream()). */
+int gh_ctx_set_stream(gh_ctx* ctx, void* stream);
+int gh_ctx_synchronize(gh_ctx* ctx);
+/* Number of kernels this context has launched (bench `gpu_launches`). */
+int gh_ctx_launch_count(gh_ctx* ctx, int64_t* count);
+/* Per-kernel CUDA-event timing on the context stream (off by default).
+ * gh_ctx_kernel_time synchronises, then reports the accumulated device time
+ * and launch count of kernels named `name` ("fft", "synth_fft", "gather",
+ * "decode", "convert", "direct_simt", "direct_umma", "synth") since the last
+ * reset. */
+int gh_ctx_set_timing(gh_ctx* ctx, int32_t on);
+int gh_ctx_kernel_time(gh_ctx* ctx, const char* name, double* total_ms, int64_t* count);
+int gh_ctx_reset_timing(gh_ctx* ctx);
+/* Diagnostics: measured shared-memory (LSU) read bandwidth of the device,
+ * GB/s, all SMs — the roofline denominator of the gather kernel. */
+int gh_measure_smem_peak(gh_ctx* ctx, double* gbps);
+
+/* ---- mapping operator (offline) --------------------------------------- */
+/* precompute_hop_table (src/interp.cpp:156-223) on the device in fp64.
+ * wrap = 0 keeps the reference's window check (GH_ERUNTIME naming the
+ * offending bins, interp.cpp:182-201); wrap = 1 relies on the atoms'
+ * periodicity (interp.cpp:39-44) for aliasing scenes (BASELINE c1/c2). */
+int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                   int32_t scheme, int32_t wrap, gh_table** out);
+/* load_hop_table (src/interp.cpp:318-389) analogue: host arrays in the
+ * reference layout [bin][pair][K] (HopTable::entry_offset, interp.hpp:55-59);
+ * coef = complex128 (re, im) pairs, NULL means all ones (K = 1). */
+int gh_table_upload(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                    int32_t scheme, const uint32_t* idx, const double* coef,
+                    gh_table** out);
+int gh_table_info(const gh_table* t, int64_t* n_bins, int32_t* n_pairs,
+                  int32_t* k, int32_t* n_fft, double* max_residual);
+/* Copy the operator back in the reference layout (host pointers). */
+int gh_table_download(gh_table* t, uint32_t* idx, double* coef);
+int gh_table_destroy(gh_table* t);
+
+/* ---- stage kernels (device pointers) ---------------------------------- */
+/* synthesize_frame + add_noise (src/synth.cpp:15-49) for trials
+ * [trial0, trial0+T): frames complex64 [T][P][N]; truth fp64 [T][K][3]
+ * (nullable). Same counter-based draws as the oracle. */
+int gh_synth_d(gh_ctx* ctx, const gh_wave* wave, const gh_campaign* camp,
+               uint64_t trial0, int32_t n_trials, int32_t wrap, float* frames_d,
+               double* truth_d);
+/* fast_time_spectra (src/hopping.cpp:121-129): zero-padded forward FFT,
+ * complex64 [T][P][N] -> complex64 [T][P][M]. */
+int gh_spectra_d(gh_ctx* ctx, const float* frames_d, int32_t n_trials,
+                 int32_t n_pairs, int32_t n_samples, int32_t os_range,
+                 float* spectra_d);
+/* hop_decision_map (src/hopping.cpp:179-183), parity mode: complex64 frames
+ * [T][P][N] -> fp32 maps [T][G]. */
+int gh_hop_map_d(gh_ctx* ctx, gh_table* t, const float* frames_d,
+                 int32_t n_trials, int32_t combine, float* map_d);
+/* hop_estimate location stage (src/hopping.cpp:238-267) batched over
+ * trials, FFT -> gather -> argmax fused: per-trial bin index (first strict
+ * maximum, argmax_index src/direct.cpp:55-62) and its value. */
+int gh_hop_argmax_d(gh_ctx* ctx, gh_table* t, const float* frames_d,
+                    int32_t n_trials, int32_t combine, int64_t* idx_d,
+                    float* val_d);
+/* Same, from HOST complex128 frames [T][P][N] (the reference's FrameSet
+ * element type) to HOST results; copies are inside the call. */
+int gh_hop_estimate(gh_ctx* ctx, gh_table* t, const double* frames,
+                    int32_t n_trials, int32_t combine, int64_t* idx,
+                    double* val);
+/* Monte-Carlo campaign step (src/montecarlo.cpp:140-175, hop arm): synth
+ * fused into the FFT, then gather + argmax; nothing but results touch HBM. */
+int gh_campaign_hop_d(gh_ctx* ctx, gh_table* t, const gh_campaign* camp,
+                      uint64_t trial0, int32_t n_trials, int32_t combine,
+                      int64_t* idx_d, float* val_d);
+/* location_decision_map (src/direct.cpp:90-144) for T trials at once as the
+ * complex contraction Z_p = Y_p (T x N) . A_p^H (N x G) on the tensor cores
+ * (tcgen05, 3xTF32), |.|^2 summed over pairs in the epilogue. */
+int gh_direct_map_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                    const float* frames_d, int32_t n_trials, int32_t combine,
+                    float* map_d);
+/* direct_estimate location stage (src/direct.cpp:230-239): per-trial argmax
+ * fused into the contraction epilogue. */
+int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                       const float* frames_d, int32_t n_trials, int32_t combine,
+                       int64_t* idx_d, float* val_d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

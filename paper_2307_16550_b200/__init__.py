@@ -1,0 +1,21 @@
+"""B200-native (sm_100a) grid-hopping location estimation.
+
+The hot path of arXiv 2307.16550 (Grid Hopping): zero-padded range FFT,
+gather-accumulate through the location->range-bin mapping operator,
+interpolation-hopping combine, fused argmax, and the direct method's dense
+contraction — hand-written CUDA behind the C ABI in include/gridhop_b200.h.
+"""
+from . import scene
+from .scene import Scene, baseline, small
+from .api import (Context, HopTable, InvalidArgument, GridhopRuntimeError, DomainError, CudaError,
+                  precompute_hop_table, upload_hop_table, synthesize, fast_time_spectra,
+                  hop_decision_map, hop_argmax, hop_estimate, campaign_hop,
+                  location_decision_map, direct_argmax, argmax_index, lib, exported_symbols)
+
+__all__ = [
+    "scene", "Scene", "baseline", "small", "Context", "HopTable", "InvalidArgument",
+    "GridhopRuntimeError", "DomainError", "CudaError", "precompute_hop_table",
+    "upload_hop_table", "synthesize", "fast_time_spectra", "hop_decision_map", "hop_argmax",
+    "hop_estimate", "campaign_hop", "location_decision_map", "direct_argmax", "argmax_index",
+    "lib", "exported_symbols",
+]

@@ -1,0 +1,347 @@
+"""Python host mirror of the reference estimator interfaces over the C ABI.
+
+Names follow the reference library (include/gridhop/{hopping,direct,interp,
+synth,montecarlo}.hpp); arrays on the device are torch tensors (torch is
+only the device-memory / stream plumbing), host arrays are numpy. Every call
+goes through libgridhop_b200.so; there is no CPU fallback — a missing or
+unloadable library raises at import time.
+
+Error behaviour mirrors the reference's exception types:
+  GH_EINVAL   -> InvalidArgument (ValueError)      std::invalid_argument
+  GH_ERUNTIME -> GridhopRuntimeError (RuntimeError) std::runtime_error
+  GH_EDOMAIN  -> DomainError (ArithmeticError)      std::domain_error
+  GH_ECUDA    -> CudaError (RuntimeError)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+
+from .scene import CCampaign, CGrid, CWave, Scene, POWER
+
+LIB_PATH = Path(__file__).resolve().parent / "libgridhop_b200.so"
+HEADER = Path(__file__).resolve().parent.parent / "include" / "gridhop_b200.h"
+
+
+class InvalidArgument(ValueError):
+    pass
+
+
+class GridhopRuntimeError(RuntimeError):
+    pass
+
+
+class DomainError(ArithmeticError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_EXC = {1: InvalidArgument, 2: GridhopRuntimeError, 3: DomainError, 4: CudaError}
+
+_lib = None
+
+
+def exported_symbols() -> list[str]:
+    """Function names declared in include/gridhop_b200.h."""
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(gh_[a-z0-9_]+)\s*\(", txt)))
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build()")
+        L = C.CDLL(str(LIB_PATH))
+        vp, i32, i64, u64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
+        P = C.POINTER
+        sig = {
+            "gh_last_error": (C.c_char_p, []),
+            "gh_abi_version": (C.c_int, []),
+            "gh_ctx_create": (C.c_int, [i32, P(vp)]),
+            "gh_ctx_destroy": (C.c_int, [vp]),
+            "gh_ctx_get_stream": (C.c_int, [vp, P(vp)]),
+            "gh_ctx_set_stream": (C.c_int, [vp, vp]),
+            "gh_ctx_synchronize": (C.c_int, [vp]),
+            "gh_ctx_launch_count": (C.c_int, [vp, P(i64)]),
+            "gh_ctx_set_timing": (C.c_int, [vp, i32]),
+            "gh_ctx_kernel_time": (C.c_int, [vp, C.c_char_p, P(f64), P(i64)]),
+            "gh_ctx_reset_timing": (C.c_int, [vp]),
+            "gh_measure_smem_peak": (C.c_int, [vp, P(f64)]),
+            "gh_table_build": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, P(vp)]),
+            "gh_table_upload": (C.c_int, [vp, P(CWave), P(CGrid), i32, vp, vp, P(vp)]),
+            "gh_table_info": (C.c_int, [vp, P(i64), P(i32), P(i32), P(i32), P(f64)]),
+            "gh_table_download": (C.c_int, [vp, vp, vp]),
+            "gh_table_destroy": (C.c_int, [vp]),
+            "gh_synth_d": (C.c_int, [vp, P(CWave), P(CCampaign), u64, i32, i32, vp, vp]),
+            "gh_spectra_d": (C.c_int, [vp, vp, i32, i32, i32, i32, vp]),
+            "gh_hop_map_d": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+            "gh_hop_argmax_d": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
+            "gh_hop_estimate": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
+            "gh_campaign_hop_d": (C.c_int, [vp, vp, P(CCampaign), u64, i32, i32, vp, vp]),
+            "gh_direct_map_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp]),
+            "gh_direct_argmax_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        msg = lib().gh_last_error().decode()
+        raise _EXC.get(status, RuntimeError)(msg)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Context:
+    """gh_ctx: one device, one stream, scratch buffers."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().gh_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if self.h:
+            _check(lib().gh_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream_ptr(self) -> int:
+        s = C.c_void_p()
+        _check(lib().gh_ctx_get_stream(self.h, C.byref(s)))
+        return int(s.value or 0)
+
+    def torch_stream(self):
+        torch = _torch()
+        return torch.cuda.ExternalStream(self.stream_ptr, device=f"cuda:{self.device}")
+
+    def synchronize(self) -> None:
+        _check(lib().gh_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        n = C.c_int64()
+        _check(lib().gh_ctx_launch_count(self.h, C.byref(n)))
+        return int(n.value)
+
+    def set_timing(self, on: bool) -> None:
+        _check(lib().gh_ctx_set_timing(self.h, int(on)))
+
+    def reset_timing(self) -> None:
+        _check(lib().gh_ctx_reset_timing(self.h))
+
+    def smem_peak_gbps(self) -> float:
+        v = C.c_double()
+        _check(lib().gh_measure_smem_peak(self.h, C.byref(v)))
+        return v.value
+
+    def kernel_time(self, name: str):
+        """(total ms, launches) of kernels `name` since the last reset."""
+        ms, n = C.c_double(), C.c_int64()
+        _check(lib().gh_ctx_kernel_time(self.h, name.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, int(n.value)
+
+
+class HopTable:
+    """Device-resident mapping operator (HopTable, include/gridhop/interp.hpp:44-60)."""
+
+    def __init__(self, ctx: Context, scene: Scene, handle: C.c_void_p):
+        self.ctx, self.scene, self.h = ctx, scene, handle
+        G, P, K, M, res = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_double()
+        _check(lib().gh_table_info(handle, C.byref(G), C.byref(P), C.byref(K), C.byref(M),
+                                   C.byref(res)))
+        self.n_bins, self.n_pairs, self.k, self.n_fft = G.value, P.value, K.value, M.value
+        self.max_residual = res.value
+
+    def close(self) -> None:
+        if self.h:
+            _check(lib().gh_table_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def download(self):
+        """(indices uint32 [G,P,K], coeffs complex128 [G,P,K]) in the reference layout."""
+        n = self.n_bins * self.n_pairs * self.k
+        idx = np.empty(n, dtype=np.uint32)
+        coef = np.empty(2 * n, dtype=np.float64)
+        _check(lib().gh_table_download(self.h, idx.ctypes.data, coef.ctypes.data))
+        shape = (self.n_bins, self.n_pairs, self.k)
+        return idx.reshape(shape), coef.view(np.complex128).reshape(shape)
+
+
+def precompute_hop_table(ctx: Context, scene: Scene, scheme: int | None = None,
+                         wrap: bool | None = None) -> HopTable:
+    """precompute_hop_table (src/interp.cpp:156-223), built on the device in fp64."""
+    h = C.c_void_p()
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_table_build(ctx.h, C.byref(w), C.byref(g),
+                                scene.scheme if scheme is None else scheme,
+                                int(scene.wrap if wrap is None else wrap), C.byref(h)))
+    return HopTable(ctx, scene, h)
+
+
+def upload_hop_table(ctx: Context, scene: Scene, scheme: int, idx: np.ndarray,
+                     coef: np.ndarray | None) -> HopTable:
+    """load_hop_table analogue: a host table in the reference layout [G][P][K]."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    cptr = None
+    if coef is not None:
+        coef = np.ascontiguousarray(coef, dtype=np.complex128)
+        cptr = coef.ctypes.data
+    h = C.c_void_p()
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_table_upload(ctx.h, C.byref(w), C.byref(g), scheme, idx.ctypes.data, cptr,
+                                 C.byref(h)))
+    return HopTable(ctx, scene, h)
+
+
+def _as_float_frames(frames):
+    torch = _torch()
+    if frames.dtype != torch.complex64 or not frames.is_cuda or not frames.is_contiguous():
+        raise InvalidArgument("frames must be a contiguous CUDA complex64 tensor [T, P, N]")
+    return frames
+
+
+def synthesize(ctx: Context, scene: Scene, trial0: int, n_trials: int, snr_db=None,
+               wrap: bool | None = None):
+    """synthesize_frame + add_noise (src/synth.cpp:15-49) for a batch of trials.
+
+    Returns (frames complex64 [T, P, N], truth float64 [T, K, 3]) on the device."""
+    torch = _torch()
+    dev = f"cuda:{ctx.device}"
+    frames = torch.empty((n_trials, scene.n_pairs, scene.n_samples), dtype=torch.complex64, device=dev)
+    truth = torch.empty((n_trials, scene.n_targets, 3), dtype=torch.float64, device=dev)
+    w, camp = scene.c_wave(), scene.c_campaign(snr_db)
+    _check(lib().gh_synth_d(ctx.h, C.byref(w), C.byref(camp), trial0, n_trials,
+                            int(scene.wrap if wrap is None else wrap), _ptr(frames), _ptr(truth)))
+    return frames, truth
+
+
+def fast_time_spectra(ctx: Context, frames, os_range: int):
+    """fast_time_spectra (src/hopping.cpp:121-129): [T, P, N] -> [T, P, os*N]."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    T, P, N = frames.shape
+    out = torch.empty((T, P, N * os_range), dtype=torch.complex64, device=frames.device)
+    _check(lib().gh_spectra_d(ctx.h, _ptr(frames), T, P, N, os_range, _ptr(out)))
+    return out
+
+
+def hop_decision_map(ctx: Context, table: HopTable, frames, combine: int = POWER):
+    """hop_decision_map (src/hopping.cpp:179-183) for T trials: fp32 [T, G]."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    out = torch.empty((frames.shape[0], table.n_bins), dtype=torch.float32, device=frames.device)
+    _check(lib().gh_hop_map_d(ctx.h, table.h, _ptr(frames), frames.shape[0], combine, _ptr(out)))
+    return out
+
+
+def hop_argmax(ctx: Context, table: HopTable, frames, combine: int = POWER):
+    """hop_estimate location stage (src/hopping.cpp:238-267) batched: (idx, value)."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    T = frames.shape[0]
+    idx = torch.empty(T, dtype=torch.int64, device=frames.device)
+    val = torch.empty(T, dtype=torch.float32, device=frames.device)
+    _check(lib().gh_hop_argmax_d(ctx.h, table.h, _ptr(frames), T, combine, _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def hop_estimate(ctx: Context, table: HopTable, frames: np.ndarray, combine: int = POWER,
+                 out_idx: np.ndarray | None = None, out_val: np.ndarray | None = None):
+    """Host-buffer hop estimate: complex128 frames [T, P, N] -> (idx int64, value f64)."""
+    frames = np.ascontiguousarray(frames, dtype=np.complex128)
+    T = frames.shape[0]
+    if frames.ndim != 3 or frames.shape[1] != table.n_pairs or frames.shape[2] != table.scene.n_samples:
+        raise InvalidArgument("hop: frame shape mismatch")
+    idx = np.empty(T, dtype=np.int64) if out_idx is None else out_idx
+    val = np.empty(T, dtype=np.float64) if out_val is None else out_val
+    _check(lib().gh_hop_estimate(ctx.h, table.h, frames.ctypes.data, T, combine,
+                                 idx.ctypes.data, val.ctypes.data))
+    return idx, val
+
+
+def hop_estimate_ptr(ctx: Context, table: HopTable, frames_ptr: int, n_trials: int,
+                     combine: int, idx_ptr: int, val_ptr: int) -> None:
+    """Raw-pointer form (pinned host buffers from the bench)."""
+    _check(lib().gh_hop_estimate(ctx.h, table.h, frames_ptr, n_trials, combine, idx_ptr, val_ptr))
+
+
+def campaign_hop(ctx: Context, table: HopTable, scene: Scene, trial0: int, n_trials: int,
+                 combine: int = POWER, snr_db=None, out=None):
+    """One Monte-Carlo step of the hop arm (src/montecarlo.cpp:140-175):
+    synthesis fused into the FFT, gather, argmax. Returns (idx, value)."""
+    torch = _torch()
+    dev = f"cuda:{ctx.device}"
+    if out is None:
+        idx = torch.empty(n_trials, dtype=torch.int64, device=dev)
+        val = torch.empty(n_trials, dtype=torch.float32, device=dev)
+    else:
+        idx, val = out
+    camp = scene.c_campaign(snr_db)
+    _check(lib().gh_campaign_hop_d(ctx.h, table.h, C.byref(camp), trial0, n_trials, combine,
+                                   _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def location_decision_map(ctx: Context, scene: Scene, frames, combine: int = POWER):
+    """location_decision_map (src/direct.cpp:90-144) for T trials: fp32 [T, G]."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    out = torch.empty((frames.shape[0], scene.n_bins), dtype=torch.float32, device=frames.device)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_direct_map_d(ctx.h, C.byref(w), C.byref(g), _ptr(frames), frames.shape[0],
+                                 combine, _ptr(out)))
+    return out
+
+
+def direct_argmax(ctx: Context, scene: Scene, frames, combine: int = POWER):
+    """direct_estimate location stage (src/direct.cpp:230-239) batched: (idx, value)."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    T = frames.shape[0]
+    idx = torch.empty(T, dtype=torch.int64, device=frames.device)
+    val = torch.empty(T, dtype=torch.float32, device=frames.device)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_direct_argmax_d(ctx.h, C.byref(w), C.byref(g), _ptr(frames), T, combine,
+                                    _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def argmax_index(values) -> int:
+    """argmax_index (src/direct.cpp:55-62): first strict maximum."""
+    v = np.asarray(values)
+    if v.size == 0:
+        raise InvalidArgument("argmax of empty scan")
+    return int(np.argmax(v))  # numpy returns the first occurrence of the max

@@ -1,0 +1,550 @@
+// gh_api.cu — the extern "C" boundary (include/gridhop_b200.h).
+//
+// Every entry point runs its body under `guarded`, which maps gh::Error
+// codes (and any other exception) onto the int status + thread-local message
+// convention. Validation messages follow the reference's exception texts
+// (src/hopping.cpp:17-23, 243-251; src/interp.cpp:156-201; src/model.cpp:50).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "gh_internal.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return GH_OK;
+  } catch (const gh::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return GH_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GH_ERUNTIME;
+  }
+}
+
+using gh::fail;
+
+void use_device(gh::Ctx* c) { GH_CUDA(cudaSetDevice(c->device)); }
+
+void check_wave(const gh_wave* w) {
+  if (!w) fail(GH_EINVAL, "waveform: null descriptor");
+  if (w->n_samples < 2) fail(GH_EINVAL, "waveform: n_samples must be >= 2");
+  if (w->os_range < 1) fail(GH_EINVAL, "hop table: oversampling must be >= 1");
+  if (!(w->range_scale > 0.0) || !std::isfinite(w->range_scale))
+    fail(GH_EINVAL, "waveform: bandwidth must be positive");
+  if (w->n_pairs < 1) fail(GH_EINVAL, "geometry: at least one TX-RX pair required");
+  if (!w->tx || !w->rx) fail(GH_EINVAL, "geometry: null station arrays");
+  for (int i = 0; i < 3 * w->n_pairs; ++i)
+    if (!std::isfinite(w->tx[i]) || !std::isfinite(w->rx[i]))
+      fail(GH_EINVAL, "geometry: receiver position must be finite");
+}
+
+int64_t grid_size(const gh_grid* g) {
+  if (!g) fail(GH_EINVAL, "grid: null descriptor");
+  for (int d = 0; d < 3; ++d)
+    if (g->n[d] < 1) fail(GH_EINVAL, "hop table: empty grid");
+  return (int64_t)g->n[0] * g->n[1] * g->n[2];
+}
+
+double* upload_txrx(gh::Ctx* c, const gh_wave* w, gh::Buffer& buf) {
+  std::vector<double> h(static_cast<size_t>(w->n_pairs) * 6);
+  for (int p = 0; p < w->n_pairs; ++p)
+    for (int d = 0; d < 3; ++d) {
+      h[static_cast<size_t>(p) * 6 + d] = w->tx[3 * p + d];
+      h[static_cast<size_t>(p) * 6 + 3 + d] = w->rx[3 * p + d];
+    }
+  double* d = static_cast<double*>(buf.get(sizeof(double) * h.size()));
+  GH_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c->stream));
+  GH_CUDA(cudaStreamSynchronize(c->stream));
+  return d;
+}
+
+gh::Table* new_table(gh::Ctx* c, const gh_wave* w, const gh_grid* g, int scheme) {
+  check_wave(w);
+  const int64_t G = grid_size(g);
+  if (scheme < GH_NEAREST || scheme > GH_POLAR) fail(GH_EINVAL, "unknown interpolation scheme");
+  auto* t = new gh::Table();
+  t->ctx = c;
+  t->scheme = scheme;
+  t->K = scheme == GH_NEAREST ? 1 : (scheme == GH_LINEAR ? 2 : 3);
+  t->G = G;
+  t->P = w->n_pairs;
+  t->N = w->n_samples;
+  t->os = w->os_range;
+  t->M = w->n_samples * w->os_range;
+  t->scale = w->range_scale;
+  t->grid = *g;
+  t->tx.assign(w->tx, w->tx + 3 * w->n_pairs);
+  t->rx.assign(w->rx, w->rx + 3 * w->n_pairs);
+  std::vector<double> h(static_cast<size_t>(t->P) * 6);
+  for (int p = 0; p < t->P; ++p)
+    for (int d = 0; d < 3; ++d) {
+      h[static_cast<size_t>(p) * 6 + d] = w->tx[3 * p + d];
+      h[static_cast<size_t>(p) * 6 + 3 + d] = w->rx[3 * p + d];
+    }
+  GH_CUDA(cudaMalloc(&t->txrx_d, sizeof(double) * h.size()));
+  GH_CUDA(cudaMemcpy(t->txrx_d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  return t;
+}
+
+void free_table(gh::Table* t) {
+  if (!t) return;
+  cudaFree(t->txrx_d);
+  cudaFree(t->idx_d);
+  cudaFree(t->coef_d);
+  cudaFree(t->plan.tiles_d);
+  cudaFree(t->plan.win_d);
+  cudaFree(t->plan.rows_d);
+  cudaFree(t->plan.coef3_d);
+  delete t;
+}
+
+void check_combine(int combine) {
+  if (combine != GH_POWER && combine != GH_MAGNITUDE) fail(GH_EINVAL, "combine: unknown mode");
+}
+
+// spectra in the gather layout for table t, from frames or from synthesis
+void* gather_spectra(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp,
+                     int T, int combine) {
+  gh::build_plan(c, t);
+  const gh::Plan& pl = t->plan;
+  const int n_tb = (T + pl.tb - 1) / pl.tb;
+  const size_t bytes = static_cast<size_t>(n_tb) * t->P * t->M * pl.tb * pl.esize;
+  void* spec = c->spectra.get(bytes);
+  const int kind = pl.k3 ? gh::FFT_GATHER_COMPLEX
+                         : (combine == GH_MAGNITUDE ? gh::FFT_GATHER_MAG : gh::FFT_GATHER_POWER);
+  gh::launch_fft(c, frames, sp, T, t->P, t->N, t->os, pl.tb, kind, spec);
+  return spec;
+}
+
+void hop_argmax(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
+                int combine, int64_t* idx_d, float* val_d) {
+  void* spec = gather_spectra(c, t, frames, sp, T, combine);
+  auto* keys = static_cast<unsigned long long*>(c->keys.get(sizeof(unsigned long long) * T));
+  GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * T, c->stream));
+  gh::launch_gather(c, t, spec, T, combine, nullptr, keys);
+  gh::launch_decode_keys(c, keys, T, idx_d, val_d);
+}
+
+gh::SynthParams make_synth(gh::Ctx* c, const double* txrx_d, double scale, const gh_campaign* camp,
+                           uint64_t trial0, int wrap) {
+  if (!camp) fail(GH_EINVAL, "campaign: null descriptor");
+  if (camp->n_targets < 1 || camp->n_targets > 8)
+    fail(GH_EINVAL, "campaign: n_targets must be in [1, 8]");
+  if (camp->dims != 2 && camp->dims != 3) fail(GH_EINVAL, "campaign: dims must be 2 or 3");
+  if (camp->amp_mode < 0 || camp->amp_mode > 3) fail(GH_EINVAL, "campaign: unknown amp_mode");
+  if (camp->snr_mode < 0 || camp->snr_mode > 2) fail(GH_EINVAL, "campaign: unknown snr_mode");
+  gh::SynthParams sp{};
+  sp.txrx_d = txrx_d;
+  sp.scale = scale;
+  sp.camp = *camp;
+  sp.trial0 = trial0;
+  sp.wrap = wrap;
+  sp.err_flag_d = static_cast<int*>(c->misc.get(sizeof(int)));
+  GH_CUDA(cudaMemsetAsync(sp.err_flag_d, 0, sizeof(int), c->stream));
+  return sp;
+}
+
+void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
+  int h = 0;
+  GH_CUDA(cudaMemcpyAsync(&h, sp.err_flag_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  GH_CUDA(cudaStreamSynchronize(c->stream));
+  if (h & 2) fail(GH_EDOMAIN, "degenerate geometry: target coincides with a station");
+  if (h & 1) fail(GH_ERUNTIME, "scene outside unambiguous window");
+}
+
+__global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = in[i];
+    out[i] = make_float2((float)v.x, (float)v.y);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gh_last_error(void) { return g_err.c_str(); }
+int gh_abi_version(void) { return GH_ABI_VERSION; }
+
+int gh_ctx_create(int32_t device, gh_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(GH_EINVAL, "ctx: null output");
+    int n = 0;
+    GH_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) fail(GH_EINVAL, "ctx: no such CUDA device");
+    GH_CUDA(cudaSetDevice(device));
+    auto* c = new gh::Ctx();
+    c->device = device;
+    GH_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    GH_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    int optin = 0;
+    GH_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    c->smem_optin = static_cast<size_t>(optin);
+    *out = reinterpret_cast<gh_ctx*>(c);
+  });
+}
+
+int gh_ctx_destroy(gh_ctx* ctx) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->spectra.release();
+    c->frames.release();
+    c->keys.release();
+    c->misc.release();
+    c->twiddle_buf.release();
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int gh_ctx_get_stream(gh_ctx* ctx, void** stream) {
+  return guarded([&] {
+    if (!ctx || !stream) fail(GH_EINVAL, "ctx: null argument");
+    *stream = reinterpret_cast<gh::Ctx*>(ctx)->stream;
+  });
+}
+
+int gh_ctx_set_stream(gh_ctx* ctx, void* stream) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    use_device(c);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) GH_CUDA(cudaStreamDestroy(c->stream));
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->own_stream = false;
+  });
+}
+
+int gh_ctx_synchronize(gh_ctx* ctx) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    use_device(c);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_ctx_launch_count(gh_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    if (!ctx || !count) fail(GH_EINVAL, "ctx: null argument");
+    *count = reinterpret_cast<gh::Ctx*>(ctx)->launches;
+  });
+}
+
+int gh_ctx_set_timing(gh_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    c->timing = on != 0;
+  });
+}
+
+int gh_ctx_kernel_time(gh_ctx* ctx, const char* name, double* total_ms, int64_t* count) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !name) fail(GH_EINVAL, "ctx: null argument");
+    use_device(c);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->pending) {
+      float ms = 0.f;
+      GH_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      auto it = std::find_if(c->times.begin(), c->times.end(),
+                             [&](const auto& kv) { return kv.first == p.name; });
+      if (it == c->times.end()) {
+        c->times.push_back({p.name, gh::KernelTimes{}});
+        it = c->times.end() - 1;
+      }
+      it->second.ms += ms;
+      it->second.count += 1;
+      c->event_pool.push_back(p.a);
+      c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+    double ms = 0.0;
+    int64_t n = 0;
+    for (const auto& kv : c->times)
+      if (kv.first == name) {
+        ms = kv.second.ms;
+        n = kv.second.count;
+      }
+    if (total_ms) *total_ms = ms;
+    if (count) *count = n;
+  });
+}
+
+int gh_ctx_reset_timing(gh_ctx* ctx) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    use_device(c);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->pending) {
+      c->event_pool.push_back(p.a);
+      c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+    c->times.clear();
+  });
+}
+
+int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_t scheme,
+                   int32_t wrap, gh_table** out) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !out) fail(GH_EINVAL, "hop table: null argument");
+    use_device(c);
+    gh::Table* t = new_table(c, wave, grid, scheme);
+    try {
+      gh::build_table_device(c, t, wrap);
+      gh::build_plan(c, t);
+    } catch (...) {
+      free_table(t);
+      throw;
+    }
+    *out = reinterpret_cast<gh_table*>(t);
+  });
+}
+
+int gh_table_upload(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_t scheme,
+                    const uint32_t* idx, const double* coef, gh_table** out) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !out || !idx) fail(GH_EINVAL, "hop table: null argument");
+    use_device(c);
+    gh::Table* t = new_table(c, wave, grid, scheme);
+    try {
+      const int64_t n = t->G * t->P * t->K;
+      for (int64_t i = 0; i < n; ++i)
+        if (idx[i] >= static_cast<uint32_t>(t->M))
+          fail(GH_ERUNTIME, "hop table: index " + std::to_string(idx[i]) + " outside the FFT grid");
+      std::vector<double2> cf(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i)
+        cf[static_cast<size_t>(i)] = coef ? make_double2(coef[2 * i], coef[2 * i + 1])
+                                          : make_double2(1.0, 0.0);
+      GH_CUDA(cudaMalloc(&t->idx_d, sizeof(uint32_t) * n));
+      GH_CUDA(cudaMalloc(&t->coef_d, sizeof(double2) * n));
+      GH_CUDA(cudaMemcpy(t->idx_d, idx, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+      GH_CUDA(cudaMemcpy(t->coef_d, cf.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+      gh::build_plan(c, t);
+    } catch (...) {
+      free_table(t);
+      throw;
+    }
+    *out = reinterpret_cast<gh_table*>(t);
+  });
+}
+
+int gh_table_info(const gh_table* table, int64_t* n_bins, int32_t* n_pairs, int32_t* k,
+                  int32_t* n_fft, double* max_residual) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<const gh::Table*>(table);
+    if (!t) fail(GH_EINVAL, "hop table: null argument");
+    if (n_bins) *n_bins = t->G;
+    if (n_pairs) *n_pairs = t->P;
+    if (k) *k = t->K;
+    if (n_fft) *n_fft = t->M;
+    if (max_residual) *max_residual = t->max_residual;
+  });
+}
+
+int gh_table_download(gh_table* table, uint32_t* idx, double* coef) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!t) fail(GH_EINVAL, "hop table: null argument");
+    use_device(t->ctx);
+    const int64_t n = t->G * t->P * t->K;
+    if (idx) GH_CUDA(cudaMemcpy(idx, t->idx_d, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+    if (coef) GH_CUDA(cudaMemcpy(coef, t->coef_d, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gh_table_destroy(gh_table* table) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!t) return;
+    use_device(t->ctx);
+    cudaStreamSynchronize(t->ctx->stream);
+    free_table(t);
+  });
+}
+
+int gh_synth_d(gh_ctx* ctx, const gh_wave* wave, const gh_campaign* camp, uint64_t trial0,
+               int32_t n_trials, int32_t wrap, float* frames_d, double* truth_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !frames_d) fail(GH_EINVAL, "synth: null argument");
+    check_wave(wave);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    const gh::SynthParams sp = make_synth(c, tr, wave->range_scale, camp, trial0, wrap);
+    gh::launch_synth(c, sp, n_trials, wave->n_pairs, wave->n_samples,
+                     reinterpret_cast<float2*>(frames_d), truth_d);
+    check_synth_flag(c, sp);
+    txrx.release();
+  });
+}
+
+int gh_spectra_d(gh_ctx* ctx, const float* frames_d, int32_t n_trials, int32_t n_pairs,
+                 int32_t n_samples, int32_t os_range, float* spectra_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !frames_d || !spectra_d) fail(GH_EINVAL, "spectra: null argument");
+    if (os_range < 1) fail(GH_EINVAL, "spectra: oversampling must be >= 1");
+    if (n_pairs < 1 || n_samples < 2) fail(GH_EINVAL, "spectra: bad frame shape");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::launch_fft(c, reinterpret_cast<const float2*>(frames_d), nullptr, n_trials, n_pairs,
+                   n_samples, os_range, 16, gh::FFT_NATURAL, spectra_d);
+  });
+}
+
+int gh_hop_map_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                 int32_t combine, float* map_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || !frames_d || !map_d) fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    void* spec = gather_spectra(c, t, reinterpret_cast<const float2*>(frames_d), nullptr,
+                                n_trials, combine);
+    gh::launch_gather(c, t, spec, n_trials, combine, map_d, nullptr);
+  });
+}
+
+int gh_hop_argmax_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                    int32_t combine, int64_t* idx_d, float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || !frames_d || !idx_d || !val_d) fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    hop_argmax(c, t, reinterpret_cast<const float2*>(frames_d), nullptr, n_trials, combine, idx_d,
+               val_d);
+  });
+}
+
+int gh_hop_estimate(gh_ctx* ctx, gh_table* table, const double* frames, int32_t n_trials,
+                    int32_t combine, int64_t* idx, double* val) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || !frames || !idx || !val) fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    const int64_t n = (int64_t)n_trials * t->P * t->N;
+    // frames (complex128 as the reference's FrameSet) -> device -> complex64
+    auto* d128 = static_cast<double2*>(c->frames.get(sizeof(double2) * n + sizeof(float2) * n +
+                                                     (sizeof(int64_t) + sizeof(float)) * n_trials));
+    auto* d64 = reinterpret_cast<float2*>(d128 + n);
+    auto* didx = reinterpret_cast<int64_t*>(d64 + n);
+    auto* dval = reinterpret_cast<float*>(didx + n_trials);
+    GH_CUDA(cudaMemcpyAsync(d128, frames, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
+    {
+      gh::KTimer kt(c, "convert");
+      k_c128_to_c64<<<blocks, 256, 0, c->stream>>>(d128, d64, n);
+      GH_LAUNCHED(c);
+    }
+    hop_argmax(c, t, d64, nullptr, n_trials, combine, didx, dval);
+    std::vector<float> hv(static_cast<size_t>(n_trials));
+    GH_CUDA(cudaMemcpyAsync(idx, didx, sizeof(int64_t) * n_trials, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaMemcpyAsync(hv.data(), dval, sizeof(float) * n_trials, cudaMemcpyDeviceToHost,
+                            c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    for (int32_t i = 0; i < n_trials; ++i) val[i] = hv[static_cast<size_t>(i)];
+  });
+}
+
+int gh_campaign_hop_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp, uint64_t trial0,
+                      int32_t n_trials, int32_t combine, int64_t* idx_d, float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || !idx_d || !val_d) fail(GH_EINVAL, "campaign: null argument");
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    // wrap mode always: the table was built against the same scene
+    const gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, 1);
+    hop_argmax(c, t, nullptr, &sp, n_trials, combine, idx_d, val_d);
+  });
+}
+
+int gh_direct_map_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const float* frames_d,
+                    int32_t n_trials, int32_t combine, float* map_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !frames_d || !map_d) fail(GH_EINVAL, "decision: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    gh::direct_map_simt(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
+                        combine, map_d, nullptr);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    txrx.release();
+  });
+}
+
+int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                       const float* frames_d, int32_t n_trials, int32_t combine, int64_t* idx_d,
+                       float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !frames_d || !idx_d || !val_d) fail(GH_EINVAL, "decision: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    auto* keys = static_cast<unsigned long long*>(c->keys.get(sizeof(unsigned long long) * n_trials));
+    GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * n_trials, c->stream));
+    gh::direct_map_simt(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
+                        combine, nullptr, keys);
+    gh::launch_decode_keys(c, keys, n_trials, idx_d, val_d);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    txrx.release();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,214 @@
+// gh_internal.cuh — shared types and device helpers of the B200 grid-hopping
+// library (sm_100a). Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gridhop_b200.h"
+
+namespace gh {
+
+// ------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(GH_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define GH_CUDA(x) ::gh::check_cuda((x), #x)
+#define GH_LAUNCHED(ctx) \
+  do { ::gh::check_cuda(cudaGetLastError(), "kernel launch"); (ctx)->launches++; } while (0)
+
+// ------------------------------------------------------------ host state
+struct Buffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t n) {
+    if (n > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      GH_CUDA(cudaMalloc(&p, n));
+      bytes = n;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct KernelTimes {
+  double ms = 0.0;
+  int64_t count = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t launches = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  Buffer spectra, frames, keys, misc, twiddle_buf;
+  int twiddle_m = 0;
+  // optional per-kernel CUDA-event timing on the context stream
+  bool timing = false;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<std::pair<std::string, KernelTimes>> times;
+};
+
+// Records events around one launch when ctx->timing is set.
+struct KTimer {
+  Ctx* c;
+  const char* name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  static cudaEvent_t take(Ctx* c) {
+    if (!c->event_pool.empty()) {
+      cudaEvent_t e = c->event_pool.back();
+      c->event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  KTimer(Ctx* c_, const char* n) : c(c_), name(n) {
+    if (c->timing) {
+      a = take(c);
+      b = take(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~KTimer() {
+    if (c->timing) {
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({name, a, b});
+    }
+  }
+};
+
+// Gather plan: how a CTA stages range windows and walks location bins.
+//   full  : every (pair) window is the whole ring; CTAs cover bin chunks.
+//   tiled : location tiles (3-D boxes), per-(tile, pair) range windows.
+struct TileDesc {
+  int32_t x0, y0, z0, wx, wy, wz;
+  int64_t entry_off;  // first entry (bin) of this tile in the plan arrays
+  int32_t rows;       // staged rows in total (sum over pairs)
+  int32_t pad;
+};
+
+struct Plan {
+  bool built = false;
+  bool full = false;
+  int tb = 16;            // trials per CTA (lanes per bin)
+  int esize = 4;          // staged element bytes (float power / float2 complex)
+  int k3 = 0;             // 1: consecutive-triple combine with coefficients
+  int p4 = 4;             // pairs padded to a multiple of 4 (row array stride)
+  int64_t chunk_bins = 0; // full plan: bins per CTA column
+  int n_tiles = 0;
+  int max_rows = 0;
+  TileDesc* tiles_d = nullptr;   // tiled plan
+  int4* win_d = nullptr;         // [tiles][P] {base, len, row_start, 0}
+  uint16_t* rows_d = nullptr;    // [entries][p4] first staged row per pair
+  float2* coef3_d = nullptr;     // [entries][P][3] (k3 only)
+  int64_t n_entries = 0;
+};
+
+struct Table {
+  Ctx* ctx = nullptr;
+  int scheme = 1, K = 1;
+  int64_t G = 0;
+  int P = 0, N = 0, os = 1, M = 0;
+  double scale = 0.0;
+  gh_grid grid{};
+  std::vector<double> tx, rx;
+  double* txrx_d = nullptr;   // [P][6] tx xyz, rx xyz
+  uint32_t* idx_d = nullptr;  // [G][P][K]
+  double2* coef_d = nullptr;  // [G][P][K]
+  double max_residual = 0.0;
+  Plan plan;
+};
+
+// ------------------------------------------------------------ device helpers
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__host__ __device__ inline uint64_t substream(uint64_t seed, uint64_t a, uint64_t b) {
+  uint64_t x = splitmix64(seed ^ 0x6a09e667f3bcc909ull);
+  x = splitmix64(x + 0x9e3779b97f4a7c15ull * (a + 1));
+  x = splitmix64(x + 0xbf58476d1ce4e5b9ull * (b + 1));
+  return x;
+}
+__host__ __device__ inline double uniform01(uint64_t key, uint64_t c) {
+  const uint64_t v = splitmix64(key + 0x9e3779b97f4a7c15ull * c);
+  return static_cast<double>(v >> 11) * 0x1.0p-53;
+}
+constexpr uint64_t kSceneTag = 0x53434E;
+
+#ifdef __CUDACC__
+// Bit-exact restatement of the oracle's norm/sensed_range/grid point: every
+// product and sum rounded separately (no FMA contraction).
+__device__ inline double dnorm3(const double* a, double x0, double x1, double x2) {
+  const double dx = __dsub_rn(x0, a[0]);
+  const double dy = __dsub_rn(x1, a[1]);
+  const double dz = __dsub_rn(x2, a[2]);
+  const double s = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  return __dsqrt_rn(__dadd_rn(s, __dmul_rn(dz, dz)));
+}
+__device__ inline void dgrid_point(const gh_grid& g, int64_t k, double* o) {
+  const int64_t nx = g.n[0], ny = g.n[1];
+  const int64_t ix = k % nx, iy = (k / nx) % ny, iz = k / (nx * ny);
+  o[0] = __dadd_rn(g.origin[0], __dmul_rn(g.spacing[0], (double)ix));
+  o[1] = __dadd_rn(g.origin[1], __dmul_rn(g.spacing[1], (double)iy));
+  o[2] = __dadd_rn(g.origin[2], __dmul_rn(g.spacing[2], (double)iz));
+}
+#endif
+
+// ------------------------------------------------------------ launchers
+struct SynthParams {
+  const double* txrx_d;  // [P][6]
+  double scale;
+  gh_campaign camp;
+  uint64_t trial0;
+  int wrap;
+  int* err_flag_d;       // set to 1 on window violation (wrap = 0)
+};
+
+// spectra layouts written by the FFT kernel
+enum FftOut { FFT_NATURAL = 0, FFT_GATHER_POWER = 1, FFT_GATHER_MAG = 2, FFT_GATHER_COMPLEX = 3 };
+
+void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth,
+                int T, int P, int N, int os, int tb, int out_kind, void* out_d);
+void launch_synth(Ctx* ctx, const SynthParams& sp, int T, int P, int N, float2* frames_d,
+                  double* truth_d);
+void build_table_device(Ctx* ctx, Table* t, int wrap);
+void build_plan(Ctx* ctx, Table* t);
+void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
+                   float* map_d, unsigned long long* keys_d);
+void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
+                        int64_t* idx_d, float* val_d);
+void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                     const float2* frames_d, int T, int combine, float* map_d,
+                     unsigned long long* keys_d);
+
+}  // namespace gh

@@ -1,0 +1,603 @@
+// gh_table.cu — offline mapping operator on the device (fp64) and the gather
+// plan derived from it.
+//
+// Reference: precompute_hop_table / fit_atom (src/interp.cpp:21-223). The
+// index rules (llround / floor on the wrapped position, interp.cpp:88-111)
+// only see sensed_range, fmod and one product, all rounded individually here
+// (__dmul_rn/__dadd_rn/__dsqrt_rn) exactly as the -ffp-contract=off oracle
+// does, so indices are bit-identical; coefficients agree to ~1e-15.
+//
+// The gather plan turns the [bin][pair][K] operator into what the gather
+// kernel streams: per location tile (a 3-D box of bins) and pair, a window of
+// range rows [base, base+len) mod M staged in shared memory, and per
+// (bin, pair) the uint16 shared-memory row of its first FFT bin.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "gh_internal.cuh"
+
+namespace gh {
+namespace {
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+struct cd {
+  double re, im;
+};
+__device__ inline cd cmul(cd a, cd b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ inline cd cadd(cd a, cd b) { return {a.re + b.re, a.im + b.im}; }
+__device__ inline cd csub(cd a, cd b) { return {a.re - b.re, a.im - b.im}; }
+__device__ inline cd cconj(cd a) { return {a.re, -a.im}; }
+__device__ inline cd cdivr(cd a, double d) { return {a.re / d, a.im / d}; }
+__device__ inline cd cdiv(cd a, cd b) {
+  const double den = b.re * b.re + b.im * b.im;
+  return {(a.re * b.re + a.im * b.im) / den, (a.im * b.re - a.re * b.im) / den};
+}
+__device__ inline double cabs2(cd a) { return a.re * a.re + a.im * a.im; }
+
+// interp.cpp:21-37 atom_kernel: phasor recurrence re-seeded every 1024 steps
+__device__ cd atom_kernel(double delta, int n) {
+  const double step = kTwoPi * delta / (double)n;
+  double wi, wr;
+  sincos(step, &wi, &wr);
+  double pr = 1.0, pim = 0.0, re = 0.0, im = 0.0;
+  for (int m = 0; m < n; ++m) {
+    if ((m & 1023) == 0) sincos(step * (double)m, &pim, &pr);
+    re += pr;
+    im += pim;
+    const double nr = pr * wr - pim * wi;
+    pim = pr * wi + pim * wr;
+    pr = nr;
+  }
+  return {re, im};
+}
+
+__device__ double wrap_range(double r, int n) {  // interp.cpp:39-44
+  double w = fmod(r, (double)n);
+  if (w < 0.0) w = __dadd_rn(w, (double)n);
+  if (w >= (double)n) w = 0.0;
+  return w;
+}
+
+__device__ bool llt_solve(const cd g[3][3], const cd b[3], cd c[3]) {
+  cd L[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) L[i][j] = {0.0, 0.0};
+  for (int k = 0; k < 3; ++k) {
+    double x = g[k][k].re;
+    for (int j = 0; j < k; ++j) x -= cabs2(L[k][j]);
+    if (!(x > 0.0)) return false;
+    const double d = sqrt(x);
+    L[k][k] = {d, 0.0};
+    for (int i = k + 1; i < 3; ++i) {
+      cd s = g[i][k];
+      for (int j = 0; j < k; ++j) s = csub(s, cmul(L[i][j], cconj(L[k][j])));
+      L[i][k] = cdivr(s, d);
+    }
+  }
+  cd y[3];
+  for (int i = 0; i < 3; ++i) {
+    cd s = b[i];
+    for (int j = 0; j < i; ++j) s = csub(s, cmul(L[i][j], y[j]));
+    y[i] = cdivr(s, L[i][i].re);
+  }
+  for (int i = 2; i >= 0; --i) {
+    cd s = y[i];
+    for (int j = i + 1; j < 3; ++j) s = csub(s, cmul(cconj(L[j][i]), c[j]));
+    c[i] = cdivr(s, L[i][i].re);
+  }
+  return true;
+}
+
+__device__ void lu_solve(const cd g[3][3], const cd b[3], cd c[3]) {
+  cd a[3][4];
+  int col[3] = {0, 1, 2};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) a[i][j] = g[i][j];
+    a[i][3] = b[i];
+  }
+  for (int k = 0; k < 3; ++k) {
+    int pi = k, pj = k;
+    double best = -1.0;
+    for (int i = k; i < 3; ++i)
+      for (int j = k; j < 3; ++j) {
+        const double v = sqrt(cabs2(a[i][j]));
+        if (v > best) best = v, pi = i, pj = j;
+      }
+    for (int j = 0; j < 4; ++j) { cd t = a[k][j]; a[k][j] = a[pi][j]; a[pi][j] = t; }
+    for (int i = 0; i < 3; ++i) { cd t = a[i][k]; a[i][k] = a[i][pj]; a[i][pj] = t; }
+    { int t = col[k]; col[k] = col[pj]; col[pj] = t; }
+    if (best == 0.0) continue;
+    for (int i = k + 1; i < 3; ++i) {
+      const cd f = cdiv(a[i][k], a[k][k]);
+      for (int j = k; j < 4; ++j) a[i][j] = csub(a[i][j], cmul(f, a[k][j]));
+    }
+  }
+  cd x[3];
+  for (int i = 2; i >= 0; --i) {
+    cd s = a[i][3];
+    for (int j = i + 1; j < 3; ++j) s = csub(s, cmul(a[i][j], x[j]));
+    x[i] = (a[i][i].re == 0.0 && a[i][i].im == 0.0) ? cd{0.0, 0.0} : cdiv(s, a[i][i]);
+  }
+  for (int i = 0; i < 3; ++i) c[col[i]] = x[i];
+}
+
+// fit_atom (interp.cpp:78-154) + polar (oracle/gridhop_oracle.cpp fit_atom)
+__device__ double fit_atom(int n_samples, int os, double r, int scheme, uint32_t* idx, cd* c) {
+  const int n_fft = n_samples * os;
+  const double rw = wrap_range(r, n_samples);
+  const double pos = __dmul_rn(rw, (double)os);
+  int k = scheme == GH_NEAREST ? 1 : (scheme == GH_LINEAR ? 2 : 3);
+  for (int j = 0; j < 3; ++j) { idx[j] = 0; c[j] = {0.0, 0.0}; }
+  long long ir = llround(pos);
+  if (scheme == GH_NEAREST) {
+    idx[0] = (uint32_t)(ir % n_fft);
+    c[0] = {1.0, 0.0};
+  } else if (scheme == GH_LINEAR) {
+    const long long i0 = (long long)floor(pos);
+    const double t = __dsub_rn(pos, (double)i0);
+    idx[0] = (uint32_t)(i0 % n_fft);
+    idx[1] = (uint32_t)((i0 + 1) % n_fft);
+    c[0] = {__dsub_rn(1.0, t), 0.0};
+    c[1] = {t, 0.0};
+  } else {
+    idx[0] = (uint32_t)((ir - 1 + n_fft) % n_fft);
+    idx[1] = (uint32_t)(ir % n_fft);
+    idx[2] = (uint32_t)((ir + 1) % n_fft);
+  }
+  double rbar[3] = {0.0, 0.0, 0.0};
+  for (int j = 0; j < k; ++j) rbar[j] = (double)idx[j] / (double)os;
+  cd gram[3][3], rhs[3];
+  for (int a = 0; a < 3; ++a) {
+    rhs[a] = {0.0, 0.0};
+    for (int b = 0; b < 3; ++b) gram[a][b] = {a == b ? 1.0 : 0.0, 0.0};
+  }
+  for (int j = 0; j < k; ++j) {
+    rhs[j] = atom_kernel(rbar[j] - rw, n_samples);
+    for (int l = 0; l < k; ++l) gram[j][l] = atom_kernel(rbar[j] - rbar[l], n_samples);
+  }
+  if (scheme == GH_POLY3) {
+    if (!llt_solve(gram, rhs, c)) {
+      cd g2[3][3];
+      const double tr = gram[0][0].re + gram[1][1].re + gram[2][2].re;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) g2[a][b] = gram[a][b];
+      for (int a = 0; a < 3; ++a) g2[a][a].re += 1e-12 * tr;
+      if (!llt_solve(g2, rhs, c)) lu_solve(g2, rhs, c);
+    }
+  } else if (scheme == GH_POLAR) {
+    const double nn = (double)n_samples;
+    const double h = 1.0 / (double)os;
+    const double d1 = sqrt(fmax(0.0, 2.0 * nn - 2.0 * atom_kernel(h, n_samples).re));
+    const double d2 = sqrt(fmax(0.0, 2.0 * nn - 2.0 * atom_kernel(2.0 * h, n_samples).re));
+    double half = d2 / (2.0 * d1);
+    half = fmin(1.0, fmax(-1.0, half));
+    const double theta = 2.0 * acos(half);
+    const double t = pos - (double)ir;
+    const double ct = cos(theta * t), st = sin(theta * t);
+    const double a = (1.0 - ct) / (1.0 - cos(theta));
+    const double b = st / (2.0 * sin(theta));
+    c[0] = {0.5 * a - b, 0.0};
+    c[1] = {1.0 - a, 0.0};
+    c[2] = {0.5 * a + b, 0.0};
+  }
+  cd quad = {0.0, 0.0}, cross = {0.0, 0.0};
+  for (int j = 0; j < k; ++j) {
+    cd gc = {0.0, 0.0};
+    for (int l = 0; l < k; ++l) gc = cadd(gc, cmul(gram[j][l], c[l]));
+    quad = cadd(quad, cmul(cconj(c[j]), gc));
+    cross = cadd(cross, cmul(cconj(c[j]), rhs[j]));
+  }
+  return sqrt(fmax(0.0, (double)n_samples - 2.0 * cross.re + quad.re));
+}
+
+struct BuildArgs {
+  gh_grid grid;
+  const double* txrx;  // [P][6]
+  double scale;
+  int P, N, os, K, scheme, wrap;
+  int64_t G;
+  uint32_t* idx;
+  double2* coef;
+  uint8_t* flags;      // window (1) / degenerate (2) per entry
+  unsigned long long* max_res_bits;
+  unsigned long long* n_flag;
+};
+
+__global__ void k_build(BuildArgs a) {
+  const int64_t total = a.G * a.P;
+  double worst = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / a.P;
+    const int p = (int)(e % a.P);
+    double x[3];
+    dgrid_point(a.grid, b, x);
+    const double* tx = a.txrx + 6 * p;
+    const double dtx = dnorm3(tx, x[0], x[1], x[2]);
+    const double drx = dnorm3(tx + 3, x[0], x[1], x[2]);
+    uint8_t fl = 0;
+    if (dtx == 0.0 || drx == 0.0) fl |= 2;
+    const double r = __dmul_rn(a.scale, __dadd_rn(dtx, drx));
+    if (!a.wrap && !(r >= 0.0 && r < (double)a.N)) fl |= 1;
+    a.flags[e] = fl;
+    if (fl) atomicAdd(a.n_flag, 1ull);
+    uint32_t idx[3];
+    cd c[3];
+    const double res = fit_atom(a.N, a.os, r, a.scheme, idx, c);
+    for (int j = 0; j < a.K; ++j) {
+      a.idx[e * a.K + j] = idx[j];
+      a.coef[e * a.K + j] = make_double2(c[j].re, c[j].im);
+    }
+    worst = fmax(worst, res);
+  }
+  // residuals are >= 0: their IEEE bits order like the values
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(a.max_res_bits, (unsigned long long)__double_as_longlong(worst));
+}
+
+// smallest flagged entry index strictly above `after` (offender report)
+__global__ void k_next_flag(const uint8_t* flags, int64_t total, int64_t after,
+                            unsigned long long* out) {
+  for (int64_t e = after + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (flags[e]) {
+      atomicMin(out, (unsigned long long)e);
+      return;
+    }
+}
+
+// ---------------------------------------------------------------- plan
+
+__device__ inline void tile_bin(const TileDesc& td, const gh_grid& g, int64_t lb, int64_t* gb) {
+  const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
+  *gb = (td.x0 + lx) + (int64_t)g.n[0] * ((td.y0 + ly) + (int64_t)g.n[1] * (td.z0 + lz));
+}
+
+// per (tile, pair): floor(min u), ceil(max u), u = r * os unwrapped
+__global__ void k_tile_minmax(const TileDesc* tiles, gh_grid g, const double* txrx, double scale,
+                              int os, int P, int2* out) {
+  const TileDesc td = tiles[blockIdx.x];
+  const int64_t nb = (int64_t)td.wx * td.wy * td.wz;
+  __shared__ int smin[32], smax[32];
+  for (int p = 0; p < P; ++p) {
+    int lo = 0x7fffffff, hi = -0x7fffffff;
+    const double* tx = txrx + 6 * p;
+    for (int64_t lb = threadIdx.x; lb < nb; lb += blockDim.x) {
+      int64_t gb;
+      tile_bin(td, g, lb, &gb);
+      double x[3];
+      dgrid_point(g, gb, x);
+      const double u = scale * (dnorm3(tx, x[0], x[1], x[2]) + dnorm3(tx + 3, x[0], x[1], x[2])) * os;
+      lo = min(lo, (int)floor(u));
+      hi = max(hi, (int)ceil(u));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      smin[threadIdx.x >> 5] = lo;
+      smax[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        lo = min(lo, smin[w]);
+        hi = max(hi, smax[w]);
+      }
+      out[(int64_t)blockIdx.x * P + p] = make_int2(lo, hi);
+    }
+    __syncthreads();
+  }
+}
+
+struct FillArgs {
+  const TileDesc* tiles;  // null for the full plan
+  gh_grid grid;
+  const int4* win;        // [tiles][P] (full: [P])
+  const uint32_t* idx;    // [G][P][K]
+  const double2* coef;
+  int P, K, M, p4, k3;
+  int64_t G;
+  uint16_t* rows;
+  float2* coef3;
+  int* err;
+};
+
+// one CTA per tile (tiled) or grid-stride over bins (full)
+__global__ void k_fill_plan(FillArgs a) {
+  int64_t entry0 = 0, nb = a.G;
+  TileDesc td{};
+  const int4* win = a.win;
+  if (a.tiles) {
+    td = a.tiles[blockIdx.x];
+    entry0 = td.entry_off;
+    nb = (int64_t)td.wx * td.wy * td.wz;
+    win = a.win + (int64_t)blockIdx.x * a.P;
+  }
+  const int64_t total = nb * a.P;
+  const int64_t start = a.tiles ? threadIdx.x : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t step = a.tiles ? blockDim.x : (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = start; e < total; e += step) {
+    const int64_t lb = e / a.P;
+    const int p = (int)(e % a.P);
+    int64_t gb = entry0 + lb;
+    if (a.tiles) tile_bin(td, a.grid, lb, &gb);
+    const int4 w = win[p];
+    const int64_t at = (gb * a.P + p) * a.K;
+    const int first = (int)a.idx[at];
+    const int local = ((first - w.x) % a.M + a.M) % a.M;
+    if (local + (a.k3 ? 2 : 0) >= w.y) atomicOr(a.err, 1);
+    a.rows[(entry0 + lb) * a.p4 + p] = (uint16_t)(w.z + local);
+    if (a.k3) {
+      float2* c3 = a.coef3 + ((entry0 + lb) * a.P + p) * 3;
+      for (int j = 0; j < 3; ++j) {
+        const double2 c = j < a.K ? a.coef[at + j] : make_double2(0.0, 0.0);
+        c3[j] = make_float2((float)c.x, (float)c.y);
+      }
+    }
+  }
+}
+
+constexpr size_t kStageBudget = 216 * 1024;
+
+}  // namespace
+
+void build_table_device(Ctx* ctx, Table* t, int wrap) {
+  const int64_t total = t->G * t->P;
+  GH_CUDA(cudaMalloc(&t->idx_d, sizeof(uint32_t) * total * t->K));
+  GH_CUDA(cudaMalloc(&t->coef_d, sizeof(double2) * total * t->K));
+  uint8_t* flags = nullptr;
+  unsigned long long* scal = nullptr;  // [0] max residual bits, [1] flag count, [2] next flag
+  GH_CUDA(cudaMalloc(&flags, total));
+  GH_CUDA(cudaMalloc(&scal, 3 * sizeof(unsigned long long)));
+  GH_CUDA(cudaMemsetAsync(scal, 0, 3 * sizeof(unsigned long long), ctx->stream));
+  BuildArgs a{};
+  a.grid = t->grid;
+  a.txrx = t->txrx_d;
+  a.scale = t->scale;
+  a.P = t->P;
+  a.N = t->N;
+  a.os = t->os;
+  a.K = t->K;
+  a.scheme = t->scheme;
+  a.wrap = wrap;
+  a.G = t->G;
+  a.idx = t->idx_d;
+  a.coef = t->coef_d;
+  a.flags = flags;
+  a.max_res_bits = scal;
+  a.n_flag = scal + 1;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 127) / 128, 148LL * 64));
+  k_build<<<blocks, 128, 0, ctx->stream>>>(a);
+  GH_LAUNCHED(ctx);
+  unsigned long long h[2];
+  GH_CUDA(cudaMemcpyAsync(h, scal, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  double mr;
+  std::memcpy(&mr, &h[0], sizeof mr);
+  t->max_residual = mr;
+  std::string err;
+  int code = 0;
+  if (h[1] > 0) {
+    // name up to 8 offenders in (bin, pair) order, interp.cpp:182-201
+    std::string names;
+    int64_t after = -1;
+    bool degenerate = false;
+    for (int i = 0; i < 8; ++i) {
+      unsigned long long init = ~0ull;
+      GH_CUDA(cudaMemcpyAsync(scal + 2, &init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+      k_next_flag<<<blocks, 128, 0, ctx->stream>>>(flags, total, after, scal + 2);
+      GH_LAUNCHED(ctx);
+      unsigned long long nx;
+      GH_CUDA(cudaMemcpyAsync(&nx, scal + 2, sizeof nx, cudaMemcpyDeviceToHost, ctx->stream));
+      GH_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (nx == ~0ull) break;
+      uint8_t fl;
+      GH_CUDA(cudaMemcpy(&fl, flags + nx, 1, cudaMemcpyDeviceToHost));
+      if (fl & 2) degenerate = true;
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%s(bin %lld, rx %d)", names.empty() ? "" : ", ",
+                    (long long)(nx / t->P), (int)(nx % t->P));
+      names += buf;
+      after = (int64_t)nx;
+    }
+    if (degenerate) {
+      code = GH_EDOMAIN;
+      err = "degenerate geometry: target coincides with a station";
+    } else {
+      if (h[1] > 8) names += ", ...";
+      code = GH_ERUNTIME;
+      err = "hop table: sensed range outside [0, n_samples) at " + std::to_string(h[1]) +
+            " grid entries: " + names;
+    }
+  }
+  cudaFree(flags);
+  cudaFree(scal);
+  if (code) fail(code, err);
+}
+
+void build_plan(Ctx* ctx, Table* t) {
+  Plan& pl = t->plan;
+  if (pl.built) return;
+  const int P = t->P, M = t->M;
+  pl.k3 = t->K > 1;
+  pl.esize = pl.k3 ? 8 : 4;
+  pl.p4 = (P + 3) / 4 * 4;
+  const int ring = pl.k3 ? M + 2 : M;
+  // full plan: whole ring per pair, 16 trials per CTA
+  const size_t full_bytes = static_cast<size_t>(P) * ring * 16 * pl.esize;
+  int* err_d = nullptr;
+  GH_CUDA(cudaMalloc(&err_d, sizeof(int)));
+  GH_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), ctx->stream));
+  if (full_bytes <= kStageBudget && ring <= 65535 / P) {
+    pl.full = true;
+    pl.tb = 16;
+    pl.n_tiles = 1;
+    pl.max_rows = P * ring;
+    pl.n_entries = t->G;
+    std::vector<int4> win(static_cast<size_t>(P));
+    for (int p = 0; p < P; ++p)
+      win[static_cast<size_t>(p)] = make_int4(pl.k3 ? M - 1 : 0, ring, p * ring, 0);
+    GH_CUDA(cudaMalloc(&pl.win_d, sizeof(int4) * P));
+    GH_CUDA(cudaMemcpyAsync(pl.win_d, win.data(), sizeof(int4) * P, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    pl.full = false;
+    pl.tb = pl.k3 ? 16 : 32;
+    const int budget_rows = static_cast<int>(kStageBudget / (static_cast<size_t>(pl.tb) * pl.esize));
+    const int allow = budget_rows / P - 5;
+    if (allow < 4) fail(GH_EINVAL, "gather plan: too many pairs for one shared-memory window");
+    const gh_grid& g = t->grid;
+    const int dims = g.n[2] > 1 ? 3 : 2;
+    const double grad = 2.0 * t->scale * t->os;  // max |du/dx| per metre
+    double side = allow / (grad * std::sqrt((double)dims));
+    struct Tiling {
+      std::vector<TileDesc> tiles;
+      std::vector<int4> win;
+      int max_rows = 0;
+      int64_t entries = 0;
+    };
+    int2* mm_d = nullptr;
+    size_t mm_cap = 0;
+    TileDesc* scratch_tiles = nullptr;
+    size_t tiles_cap = 0;
+    // tile boxes of about `side` metres; windows measured on the device
+    auto try_tiling = [&](double s) {
+      Tiling tl;
+      int w[3];
+      for (int d = 0; d < 3; ++d) {
+        w[d] = g.n[d] > 1 ? std::max(1, (int)std::floor(s / g.spacing[d])) : 1;
+        w[d] = std::min(w[d], g.n[d]);
+      }
+      if (dims == 2) w[2] = 1;
+      int64_t off = 0;
+      for (int z = 0; z < g.n[2]; z += w[2])
+        for (int y = 0; y < g.n[1]; y += w[1])
+          for (int x = 0; x < g.n[0]; x += w[0]) {
+            TileDesc td{};
+            td.x0 = x;
+            td.y0 = y;
+            td.z0 = z;
+            td.wx = std::min(w[0], g.n[0] - x);
+            td.wy = std::min(w[1], g.n[1] - y);
+            td.wz = std::min(w[2], g.n[2] - z);
+            td.entry_off = off;
+            off += (int64_t)td.wx * td.wy * td.wz;
+            tl.tiles.push_back(td);
+          }
+      tl.entries = off;
+      const size_t nt = tl.tiles.size();
+      if (nt > tiles_cap) {
+        if (scratch_tiles) cudaFree(scratch_tiles);
+        GH_CUDA(cudaMalloc(&scratch_tiles, sizeof(TileDesc) * nt));
+        tiles_cap = nt;
+      }
+      if (nt * P > mm_cap) {
+        if (mm_d) cudaFree(mm_d);
+        GH_CUDA(cudaMalloc(&mm_d, sizeof(int2) * nt * P));
+        mm_cap = nt * P;
+      }
+      GH_CUDA(cudaMemcpyAsync(scratch_tiles, tl.tiles.data(), sizeof(TileDesc) * nt,
+                              cudaMemcpyHostToDevice, ctx->stream));
+      k_tile_minmax<<<static_cast<int>(nt), 256, 0, ctx->stream>>>(scratch_tiles, g, t->txrx_d,
+                                                                   t->scale, t->os, P, mm_d);
+      GH_LAUNCHED(ctx);
+      std::vector<int2> mm(nt * P);
+      GH_CUDA(cudaMemcpyAsync(mm.data(), mm_d, sizeof(int2) * mm.size(), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      GH_CUDA(cudaStreamSynchronize(ctx->stream));
+      tl.win.assign(mm.size(), make_int4(0, 0, 0, 0));
+      for (size_t ti = 0; ti < nt; ++ti) {
+        int rs = 0;
+        for (int p = 0; p < P; ++p) {
+          const int2 m = mm[ti * P + p];
+          int base = m.x - 2, len = m.y - m.x + 5;
+          if (len >= ring) {
+            base = pl.k3 ? M - 1 : 0;
+            len = ring;
+          }
+          base = ((base % M) + M) % M;
+          tl.win[ti * P + p] = make_int4(base, len, rs, 0);
+          rs += len;
+        }
+        tl.tiles[ti].rows = rs;
+        tl.max_rows = std::max(tl.max_rows, rs);
+      }
+      return tl;
+    };
+    auto fits = [&](const Tiling& tl) {
+      return tl.max_rows <= budget_rows && tl.max_rows <= 65535;
+    };
+    Tiling best = try_tiling(side);
+    for (int i = 0; i < 16 && !fits(best); ++i) {
+      side *= 0.75;
+      best = try_tiling(side);
+    }
+    if (!fits(best)) fail(GH_EINVAL, "gather plan: no tiling fits the shared-memory budget");
+    // the gradient bound is a worst case: grow while the windows still fit
+    for (int i = 0; i < 8 && best.max_rows * 10 < budget_rows * 7; ++i) {
+      if (best.tiles.size() <= 1) break;
+      side *= 1.25;
+      Tiling bigger = try_tiling(side);
+      if (!fits(bigger)) break;
+      best = std::move(bigger);
+    }
+    if (scratch_tiles) cudaFree(scratch_tiles);
+    if (mm_d) cudaFree(mm_d);
+    std::vector<TileDesc>& tiles = best.tiles;
+    std::vector<int4>& win = best.win;
+    pl.max_rows = best.max_rows;
+    pl.n_tiles = static_cast<int>(tiles.size());
+    pl.n_entries = best.entries;
+    TileDesc* tiles_d = nullptr;
+    GH_CUDA(cudaMalloc(&tiles_d, sizeof(TileDesc) * tiles.size()));
+    GH_CUDA(cudaMemcpyAsync(tiles_d, tiles.data(), sizeof(TileDesc) * tiles.size(),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    GH_CUDA(cudaMalloc(&pl.win_d, sizeof(int4) * win.size()));
+    GH_CUDA(cudaMemcpyAsync(pl.win_d, win.data(), sizeof(int4) * win.size(),
+                            cudaMemcpyHostToDevice, ctx->stream));
+    pl.tiles_d = tiles_d;
+  }
+  GH_CUDA(cudaMalloc(&pl.rows_d, sizeof(uint16_t) * pl.n_entries * pl.p4));
+  GH_CUDA(cudaMemsetAsync(pl.rows_d, 0, sizeof(uint16_t) * pl.n_entries * pl.p4, ctx->stream));
+  if (pl.k3) GH_CUDA(cudaMalloc(&pl.coef3_d, sizeof(float2) * pl.n_entries * P * 3));
+  FillArgs f{};
+  f.tiles = pl.full ? nullptr : pl.tiles_d;
+  f.grid = t->grid;
+  f.win = pl.win_d;
+  f.idx = t->idx_d;
+  f.coef = t->coef_d;
+  f.P = P;
+  f.K = t->K;
+  f.M = M;
+  f.p4 = pl.p4;
+  f.k3 = pl.k3;
+  f.G = t->G;
+  f.rows = pl.rows_d;
+  f.coef3 = pl.coef3_d;
+  f.err = err_d;
+  if (pl.full) {
+    const int blocks = static_cast<int>(std::min<int64_t>((t->G * P + 255) / 256, 148LL * 32));
+    k_fill_plan<<<blocks, 256, 0, ctx->stream>>>(f);
+  } else {
+    k_fill_plan<<<pl.n_tiles, 256, 0, ctx->stream>>>(f);
+  }
+  GH_LAUNCHED(ctx);
+  int herr = 0;
+  GH_CUDA(cudaMemcpyAsync(&herr, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(err_d);
+  if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
+  pl.built = true;
+}
+
+}  // namespace gh

@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a path through the C ABI against the fp64 oracle.
+
+Gates (BASELINE.json north_star):
+  * location-bin indices identical to the oracle on every trial except
+    documented near-ties (oracle top-2 within 1e-5 relative);
+  * maps within 1e-4 relative: max|gpu - oracle| / max|oracle| per trial;
+  * table indices bit-identical, coefficients within 1e-9.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2307_16550_b200 as gh
+from paper_2307_16550_b200 import scene as S
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+TIE_TOL = 1e-5
+
+
+def near_tie(m: np.ndarray, a: int, b: int) -> bool:
+    top = m.max()
+    return abs(m[a] - m[b]) <= TIE_TOL * abs(top)
+
+
+def assert_argmax_parity(ref_maps, idx_gpu, what=""):
+    bad = []
+    for t, m in enumerate(ref_maps):
+        a = int(np.argmax(m))
+        g = int(idx_gpu[t])
+        if a != g and not near_tie(m, a, g):
+            bad.append((t, a, g, m[a], m[g]))
+    assert not bad, f"{what}: {len(bad)} argmax mismatches (not near-ties): {bad[:5]}"
+
+
+def rel_map_err(gpu, ref):
+    err = np.abs(gpu.astype(np.float64) - ref).max(axis=1)
+    return (err / np.abs(ref).max(axis=1)).max()
+
+
+def frames_to_dev(fr):
+    return torch.from_numpy(fr.astype(np.complex64)).cuda().contiguous()
+
+
+@pytest.fixture(scope="module")
+def small_scene():
+    return S.small()
+
+
+def test_table_indices_bit_identical(ctx):
+    for scheme in (S.NEAREST, S.LINEAR, S.POLY3, S.POLAR):
+        sc = S.small(scheme=scheme, nx=17, ny=13)
+        t = gh.precompute_hop_table(ctx, sc)
+        gi, gc = t.download()
+        oi, oc, omr = O.build_table(sc)
+        assert np.array_equal(gi, oi), f"scheme {scheme}: indices differ"
+        assert np.abs(gc - oc).max() < 1e-9, f"scheme {scheme}: coefficients differ"
+        assert abs(t.max_residual - omr) <= 1e-9 * max(1.0, omr)
+
+
+def test_table_indices_baseline_c1(ctx):
+    sc = S.baseline("c1")
+    t = gh.precompute_hop_table(ctx, sc)
+    gi, _ = t.download()
+    oi, _, _ = O.build_table(sc)
+    assert np.array_equal(gi, oi)
+
+
+def test_table_window_error_names_bins(ctx):
+    sc = S.small(wrap=False, bandwidth=1e9)  # aliases: ranges leave [0, N)
+    with pytest.raises(gh.GridhopRuntimeError) as e:
+        gh.precompute_hop_table(ctx, sc)
+    assert "(bin" in str(e.value) and "hop table: sensed range outside" in str(e.value)
+    with pytest.raises(O.OracleError) as eo:
+        O.build_table(sc)
+    assert str(e.value) == str(eo.value)
+
+
+def test_synth_matches_oracle(ctx, small_scene):
+    sc = small_scene
+    fr_g, tr_g = gh.synthesize(ctx, sc, 5, 9)
+    fr_o, tr_o = O.synth(sc, 5, 9)
+    assert np.array_equal(tr_g.cpu().numpy(), tr_o)
+    assert np.abs(fr_g.cpu().numpy() - fr_o).max() < 2e-5 * np.abs(fr_o).max()
+
+
+@pytest.mark.parametrize("N,os", [(64, 4), (256, 4), (512, 2), (1024, 4), (128, 1)])
+def test_spectra_match_oracle(ctx, N, os):
+    rng = np.random.default_rng(N + os)
+    fr = (rng.standard_normal((5, 3, N)) + 1j * rng.standard_normal((5, 3, N)))
+    sp_g = gh.fast_time_spectra(ctx, frames_to_dev(fr), os).cpu().numpy()
+    sp_o = O.spectra(fr, N * os)
+    assert np.abs(sp_g - sp_o).max() < 1e-5 * np.abs(sp_o).max()
+
+
+@pytest.mark.parametrize("scheme", [S.NEAREST, S.LINEAR, S.POLY3, S.POLAR])
+@pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
+def test_hop_map_and_argmax(ctx, scheme, combine):
+    sc = S.small(scheme=scheme)
+    T = 37  # not a multiple of the 16/32-trial batch
+    fr, _ = O.synth(sc, 0, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc, magnitude=combine == S.MAGNITUDE)
+    t = gh.precompute_hop_table(ctx, sc)
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, t, fd, combine).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, val = gh.hop_argmax(ctx, t, fd, combine)
+    assert_argmax_parity(ref, idx.cpu().numpy(), f"scheme {scheme}")
+    iv = idx.cpu().numpy()
+    assert np.allclose(val.cpu().numpy(), ref[np.arange(T), iv], rtol=1e-4)
+
+
+def test_hop_tiled_plan_k1(ctx):
+    # a scene whose full ring does not fit shared memory -> tiled plan
+    sc = S.small(P=12, N=512, os=4, nx=60, ny=50, scheme=S.NEAREST)
+    T = 40
+    fr, _ = O.synth(sc, 0, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    t = gh.precompute_hop_table(ctx, sc)
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, t, fd).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, _ = gh.hop_argmax(ctx, t, fd)
+    assert_argmax_parity(ref, idx.cpu().numpy(), "tiled K=1")
+
+
+def test_hop_estimate_host_buffers(ctx, small_scene):
+    sc = small_scene
+    fr, _ = O.synth(sc, 100, 21)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    t = gh.precompute_hop_table(ctx, sc)
+    idx, val = gh.hop_estimate(ctx, t, fr)
+    assert_argmax_parity(ref, idx, "host hop_estimate")
+    with pytest.raises(gh.InvalidArgument, match="hop: frame shape mismatch"):
+        gh.hop_estimate(ctx, t, fr[:, :2])
+
+
+def test_campaign_matches_oracle_campaign(ctx):
+    sc = S.baseline("c1")
+    T = 64
+    oi, oc, _ = O.build_table(sc)
+    o_idx, o_val = O.campaign_hop(sc, oi, oc, 0, T)
+    t = gh.precompute_hop_table(ctx, sc)
+    g_idx, g_val = gh.campaign_hop(ctx, t, sc, 0, T)
+    g_idx = g_idx.cpu().numpy()
+    fr, _ = O.synth(sc, 0, T)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    assert_argmax_parity(ref, g_idx, "c1 campaign")
+    assert np.array_equal(np.argmax(ref, axis=1), o_idx)
+    assert np.allclose(g_val.cpu().numpy(), o_val, rtol=1e-4)
+
+
+@pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
+def test_direct_map_and_argmax(ctx, combine):
+    sc = S.small()
+    T = 19
+    fr, _ = O.synth(sc, 3, T)
+    ref = O.direct_map(sc, fr, magnitude=combine == S.MAGNITUDE)
+    fd = frames_to_dev(fr)
+    m = gh.location_decision_map(ctx, sc, fd, combine).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, _ = gh.direct_argmax(ctx, sc, fd, combine)
+    assert_argmax_parity(ref, idx.cpu().numpy(), "direct")
+
+
+def test_edge_cases(ctx, small_scene):
+    sc = small_scene
+    t = gh.precompute_hop_table(ctx, sc)
+    empty = torch.empty((0, sc.n_pairs, sc.n_samples), dtype=torch.complex64, device="cuda")
+    idx, val = gh.hop_argmax(ctx, t, empty)
+    assert idx.numel() == 0
+    with pytest.raises(gh.InvalidArgument, match="unknown interpolation scheme"):
+        gh.precompute_hop_table(ctx, sc, scheme=9)
+    with pytest.raises(gh.InvalidArgument, match="empty grid"):
+        gh.precompute_hop_table(ctx, sc.with_(grid_n=(0, 4, 1)))
+    # single trial
+    fr, _ = O.synth(sc, 0, 1)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    idx, _ = gh.hop_argmax(ctx, t, frames_to_dev(fr))
+    assert_argmax_parity(ref, idx.cpu().numpy(), "T=1")
