@@ -114,11 +114,20 @@ def _torch():
 class Context:
     """gh_ctx: one device, one stream, scratch buffers."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, torch_stream: bool = True):
         h = C.c_void_p()
         _check(lib().gh_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        if torch_stream:
+            # enqueue on torch's current stream so kernels are ordered with the
+            # torch ops that produce inputs / consume outputs
+            torch = _torch()
+            s = torch.cuda.current_stream(device)
+            _check(lib().gh_ctx_set_stream(h, C.c_void_p(s.cuda_stream)))
+            self._torch_stream = s
+        else:
+            self._torch_stream = None
 
     def close(self) -> None:
         if self.h:
@@ -138,6 +147,8 @@ class Context:
         return int(s.value or 0)
 
     def torch_stream(self):
+        if self._torch_stream is not None:
+            return self._torch_stream
         torch = _torch()
         return torch.cuda.ExternalStream(self.stream_ptr, device=f"cuda:{self.device}")
 

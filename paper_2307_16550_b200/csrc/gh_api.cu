@@ -392,7 +392,7 @@ int gh_synth_d(gh_ctx* ctx, const gh_wave* wave, const gh_campaign* camp, uint64
                int32_t n_trials, int32_t wrap, float* frames_d, double* truth_d) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
-    if (!c || !frames_d) fail(GH_EINVAL, "synth: null argument");
+    if (!c || (n_trials > 0 && !frames_d)) fail(GH_EINVAL, "synth: null argument");
     check_wave(wave);
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
@@ -411,7 +411,8 @@ int gh_spectra_d(gh_ctx* ctx, const float* frames_d, int32_t n_trials, int32_t n
                  int32_t n_samples, int32_t os_range, float* spectra_d) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
-    if (!c || !frames_d || !spectra_d) fail(GH_EINVAL, "spectra: null argument");
+    if (!c || (n_trials > 0 && (!frames_d || !spectra_d)))
+      fail(GH_EINVAL, "spectra: null argument");
     if (os_range < 1) fail(GH_EINVAL, "spectra: oversampling must be >= 1");
     if (n_pairs < 1 || n_samples < 2) fail(GH_EINVAL, "spectra: bad frame shape");
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
@@ -427,7 +428,8 @@ int gh_hop_map_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     auto* t = reinterpret_cast<gh::Table*>(table);
-    if (!c || !t || !frames_d || !map_d) fail(GH_EINVAL, "hop: null argument");
+    if (!c || !t || (n_trials > 0 && (!frames_d || !map_d)))
+      fail(GH_EINVAL, "hop: null argument");
     check_combine(combine);
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
@@ -443,7 +445,8 @@ int gh_hop_argmax_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     auto* t = reinterpret_cast<gh::Table*>(table);
-    if (!c || !t || !frames_d || !idx_d || !val_d) fail(GH_EINVAL, "hop: null argument");
+    if (!c || !t || (n_trials > 0 && (!frames_d || !idx_d || !val_d)))
+      fail(GH_EINVAL, "hop: null argument");
     check_combine(combine);
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
@@ -458,7 +461,8 @@ int gh_hop_estimate(gh_ctx* ctx, gh_table* table, const double* frames, int32_t 
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     auto* t = reinterpret_cast<gh::Table*>(table);
-    if (!c || !t || !frames || !idx || !val) fail(GH_EINVAL, "hop: null argument");
+    if (!c || !t || (n_trials > 0 && (!frames || !idx || !val)))
+      fail(GH_EINVAL, "hop: null argument");
     check_combine(combine);
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
@@ -492,7 +496,8 @@ int gh_campaign_hop_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp, uin
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     auto* t = reinterpret_cast<gh::Table*>(table);
-    if (!c || !t || !idx_d || !val_d) fail(GH_EINVAL, "campaign: null argument");
+    if (!c || !t || (n_trials > 0 && (!idx_d || !val_d)))
+      fail(GH_EINVAL, "campaign: null argument");
     check_combine(combine);
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
@@ -507,7 +512,8 @@ int gh_direct_map_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const
                     int32_t n_trials, int32_t combine, float* map_d) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
-    if (!c || !frames_d || !map_d) fail(GH_EINVAL, "decision: null argument");
+    if (!c || (n_trials > 0 && (!frames_d || !map_d)))
+      fail(GH_EINVAL, "decision: null argument");
     check_wave(wave);
     grid_size(grid);
     check_combine(combine);
@@ -528,7 +534,8 @@ int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                        float* val_d) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
-    if (!c || !frames_d || !idx_d || !val_d) fail(GH_EINVAL, "decision: null argument");
+    if (!c || (n_trials > 0 && (!frames_d || !idx_d || !val_d)))
+      fail(GH_EINVAL, "decision: null argument");
     check_wave(wave);
     grid_size(grid);
     check_combine(combine);

@@ -1,23 +1,25 @@
 // gh_fft.cu — beat-signal synthesis and the zero-padded range FFT (sm_100a).
 //
 // Reference: fast_time_spectra / fft_rows (src/hopping.cpp:121-129,
-// src/fft.cpp:132-146, include/gridhop/fft.hpp:7-10): out[i] =
-// sum_n y[n] exp(-j 2pi i n / M), M = os * N, forward and unnormalised.
+// src/fft.cpp:132-146, include/gridhop/fft.hpp:7-10): out[k] =
+// sum_n y[n] exp(-j 2pi k n / M), M = os * N, forward and unnormalised.
 // Synthesis restates synthesize_frame + add_noise (src/synth.cpp:15-49) and
 // sample_scene (src/montecarlo.cpp:48-66) on the counter-based stream shared
 // with the oracle.
 //
-// One CTA owns TB trials of one pair (blockIdx = (trial batch, pair)) and
-// transforms them R rows at a time in shared memory:
-//   * zero padding is pruned: with bit-reversed input order the N non-zero
-//     samples land on multiples of os, and the first log2(os) DIT stages of
-//     a block (y, 0, .., 0) just replicate y, so the load writes each sample
-//     os times and the butterflies start at half = os;
-//   * the epilogue writes the gather layout [batch][pair][M][TB] (one
-//     contiguous TB-run per range bin, TB = trials of the batch) as power,
-//     magnitude or complex, or the natural [T][P][M] layout for parity.
-// Row pitch (M + 16/R float2) makes the transposing epilogue reads
-// bank-conflict free.
+// Zero padding is pruned exactly: with k = os*m + j,
+//   X[os*m + j] = sum_{n<N} (y[n] W_M^{jn}) W_N^{mn},
+// i.e. os independent N-point FFTs of twiddled copies of the N samples; the
+// padded zeros are never touched. Each N-point FFT runs as Stockham
+// radix-16/8/4/2 passes: a thread loads R points, twiddles, does the R-point
+// DFT in registers and writes back (one shared-memory round trip and two
+// barriers per pass; N = 256 is two passes). Shared memory is padded one
+// float2 per 16 so the strided Stockham writes are bank-conflict free.
+//
+// One CTA owns TB trials of one pair (blockIdx = (trial batch, pair)),
+// R_ROWS rows at a time. The epilogue writes either the natural [T][P][M]
+// complex layout (parity) or the gather layout [batch][pair][M][TB] — one
+// contiguous TB-run per range bin — as power, magnitude or complex.
 #include <cuda_runtime.h>
 
 #include "gh_internal.cuh"
@@ -144,24 +146,140 @@ __global__ void k_synth(SynthParams sp, int T, int P, int N, float2* frames,
   }
 }
 
+// ------------------------------------------------------------ FFT core
+
+// cos / sin of 2 pi e / 16
+__device__ constexpr float kC16[16] = {1.0f, 0.92387953251f, 0.70710678118f, 0.38268343236f,
+                                       0.0f, -0.38268343236f, -0.70710678118f, -0.92387953251f,
+                                       -1.0f, -0.92387953251f, -0.70710678118f, -0.38268343236f,
+                                       0.0f, 0.38268343236f, 0.70710678118f, 0.92387953251f};
+__device__ constexpr float kS16[16] = {0.0f, 0.38268343236f, 0.70710678118f, 0.92387953251f,
+                                       1.0f, 0.92387953251f, 0.70710678118f, 0.38268343236f,
+                                       0.0f, -0.38268343236f, -0.70710678118f, -0.92387953251f,
+                                       -1.0f, -0.92387953251f, -0.70710678118f, -0.38268343236f};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+constexpr int brev_c(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b)
+    if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+  return r;
+}
+constexpr int log2_c(int v) { return v <= 1 ? 0 : 1 + log2_c(v / 2); }
+
+// forward R-point DFT in registers (radix-2 DIT, constant twiddles)
+template <int R>
+__device__ __forceinline__ void dft_reg(float2* v) {
+  constexpr int LB = log2_c(R);
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int j = brev_c(i, LB);
+    if (j > i) {
+      const float2 t = v[i];
+      v[i] = v[j];
+      v[j] = t;
+    }
+  }
+#pragma unroll
+  for (int len = 2; len <= R; len <<= 1) {
+#pragma unroll
+    for (int i = 0; i < R; i += len)
+#pragma unroll
+      for (int k = 0; k < len / 2; ++k) {
+        const int e = k * (16 / len);  // exp(-2 pi i k / len) = W16^e
+        const float2 b0 = v[i + k + len / 2];
+        float2 b;
+        if (e == 0) {
+          b = b0;
+        } else if (e == 4) {  // -i
+          b = make_float2(b0.y, -b0.x);
+        } else {
+          b = cmul(b0, make_float2(kC16[e], -kS16[e]));
+        }
+        const float2 a = v[i + k];
+        v[i + k] = make_float2(a.x + b.x, a.y + b.y);
+        v[i + k + len / 2] = make_float2(a.x - b.x, a.y - b.y);
+      }
+  }
+}
+
+__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+
 struct FftArgs {
   const float2* frames;  // [T][P][N] (or null with synth)
   SynthParams sp;
   int synth;
-  int T, P, N, M, log2n, log2m, log2os, os;
+  int T, P, N, M, os, log2os, log2n, log2m;
   int tb, rows, log2rows, pitch;
+  int npass;
+  int pass_log2r[8];     // radix (log2) of each Stockham pass
   int out_kind;
-  const float2* tw;      // exp(-2 pi i k / M), k < M/2
+  const float2* tw;      // W_M^e = exp(-2 pi i e / M), e < M (global, L1-cached)
   void* out;
 };
 
+// One Stockham pass of radix R over every (row, sub-FFT) of the CTA, out of
+// place src -> dst (ping-pong buffers: no registers live across barriers).
+// ptw: this pass's twiddles W_{Ns R}^{r k} laid out [k][r-1], so lanes with
+// consecutive k read with stride (R-1) float2 — bank-conflict free.
+template <int R>
+__device__ __forceinline__ void stockham_pass(const float2* src, float2* dst, const float2* ptw,
+                                              const FftArgs& a, int log2ns, int rows_os) {
+  constexpr int LR = log2_c(R);
+  const int log2per = a.log2n - LR;
+  const int per = 1 << log2per;
+  const int Ns = 1 << log2ns;
+  const int tasks = rows_os << log2per;
+  for (int task = threadIdx.x; task < tasks; task += kFftThreads) {
+    const int ro = task >> log2per, q = task & (per - 1);  // ro = row * os + sub
+    const int row = ro >> a.log2os, sub = ro & (a.os - 1);
+    const int base = row * a.pitch;
+    const int off = sub << a.log2n;
+    const int k = q & (Ns - 1);
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float2 x = src[base + padi(off + q + r * per)];
+      if (r > 0 && Ns > 1) x = cmul(x, ptw[k * (R - 1) + r - 1]);
+      v[r] = x;
+    }
+    dft_reg<R>(v);
+    const int o = ((q - k) << LR) + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[base + padi(off + o + (r << log2ns))] = v[r];
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kFftThreads, 1) k_fft(FftArgs a) {
-  extern __shared__ float2 sm[];
+  extern __shared__ float2 smem_dyn[];
   __shared__ RowSynth rsm[16];
+  float2* ptw = smem_dyn;                // per-pass twiddles, N - 1 entries
+  float2* buf0 = smem_dyn + a.N;         // rows x pitch, ping
+  float2* buf1 = buf0 + a.rows * a.pitch;  // pong
+  float2* sm = buf0;
   const int tb = blockIdx.x, p = blockIdx.y;
   const int R = a.rows, M = a.M, N = a.N;
-  const int halfM = M >> 1;
   const double inv_n = 1.0 / (double)N;
+  // pass tables: pass with stride Ns and radix Rp holds W_M^{r k M/(Ns Rp)}
+  // at [k][r-1] (k < Ns, 1 <= r < Rp); the first pass (Ns = 1) needs none
+  {
+    int toff = 0, lns = 0;
+    for (int ps = 0; ps < a.npass; ++ps) {
+      const int lr = a.pass_log2r[ps], rp = 1 << lr, ns = 1 << lns;
+      const int cnt = ns * (rp - 1);
+      const int step = a.log2m - lns - lr;  // M / (Ns Rp) = 2^step
+      for (int e = threadIdx.x; e < cnt; e += kFftThreads) {
+        const int k = e / (rp - 1), r = e - k * (rp - 1) + 1;
+        ptw[toff + e] = __ldg(a.tw + ((r * k) << step));
+      }
+      toff += cnt;
+      lns += lr;
+    }
+  }
   for (int g0 = 0; g0 < a.tb; g0 += R) {
     if (a.synth && threadIdx.x < R) {
       const int t = tb * a.tb + g0 + threadIdx.x;
@@ -175,11 +293,10 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft(FftArgs a) {
       }
     }
     __syncthreads();
-    // load: bit-reversed, each sample replicated over its os-block
-    for (int e = threadIdx.x; e < R * N; e += blockDim.x) {
+    // load: sample n of row r -> sub-FFT j input y[n] W_M^{jn}
+    for (int e = threadIdx.x; e < R * N; e += kFftThreads) {
       const int r = e >> a.log2n;
-      const int g = e & (N - 1);
-      const int n = a.log2n ? (int)(__brev((unsigned)g) >> (32 - a.log2n)) : 0;
+      const int n = e & (N - 1);
       const int t = tb * a.tb + g0 + r;
       float2 v = make_float2(0.f, 0.f);
       if (t < a.T) {
@@ -188,41 +305,46 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft(FftArgs a) {
         else
           v = a.frames[((int64_t)t * a.P + p) * N + n];
       }
-      float2* dst = sm + r * a.pitch + (g << a.log2os);
-      for (int j = 0; j < a.os; ++j) dst[j] = v;
+      float2* row = buf0 + r * a.pitch;
+      row[padi(n)] = v;
+      for (int j = 1; j < a.os; ++j) row[padi(j * N + n)] = cmul(v, __ldg(a.tw + j * n));
     }
     __syncthreads();
-    // radix-2 DIT stages from half = os
-    for (int half = a.os, lh = a.log2os; half < M; half <<= 1, ++lh) {
-      const int tw_step = halfM >> lh;  // M / (2 half)
-      for (int e = threadIdx.x; e < R * halfM; e += blockDim.x) {
-        const int r = e >> (a.log2m - 1);
-        const int b = e & (halfM - 1);
-        const int j = b & (half - 1);
-        const int i0 = ((b >> lh) << (lh + 1)) + j;
-        float2* x = sm + r * a.pitch;
-        const float2 w = __ldg(a.tw + j * tw_step);
-        const float2 u = x[i0], v0 = x[i0 + half];
-        const float2 v = make_float2(v0.x * w.x - v0.y * w.y, v0.x * w.y + v0.y * w.x);
-        x[i0] = make_float2(u.x + v.x, u.y + v.y);
-        x[i0 + half] = make_float2(u.x - v.x, u.y - v.y);
-      }
-      __syncthreads();
+    // N-point Stockham passes, ping-pong between buf0 and buf1
+    const int rows_os = R * a.os;
+    float2* src = buf0;
+    float2* dst = buf1;
+    int lns = 0, toff = 0;
+    for (int ps = 0; ps < a.npass; ++ps) {
+      const int lr = a.pass_log2r[ps];
+      const float2* t = ptw + toff;
+      if (lr == 4) stockham_pass<16>(src, dst, t, a, lns, rows_os);
+      else if (lr == 3) stockham_pass<8>(src, dst, t, a, lns, rows_os);
+      else if (lr == 2) stockham_pass<4>(src, dst, t, a, lns, rows_os);
+      else stockham_pass<2>(src, dst, t, a, lns, rows_os);
+      toff += (1 << lns) * ((1 << lr) - 1);
+      lns += lr;
+      float2* tmp = src;
+      src = dst;
+      dst = tmp;
     }
-    // epilogue
+    sm = src;  // result
+    // epilogue: output bin k = os * m + j lives in sub-row j at m
     if (a.out_kind == FFT_NATURAL) {
       float2* out = static_cast<float2*>(a.out);
-      for (int e = threadIdx.x; e < R * M; e += blockDim.x) {
-        const int r = e >> a.log2m, i = e & (M - 1);
+      for (int e = threadIdx.x; e < R * M; e += kFftThreads) {
+        const int r = e >> a.log2m, k = e & (M - 1);
         const int t = tb * a.tb + g0 + r;
-        if (t < a.T) out[((int64_t)t * a.P + p) * M + i] = sm[r * a.pitch + i];
+        const int j = k & (a.os - 1), m = k >> a.log2os;
+        if (t < a.T) out[((int64_t)t * a.P + p) * M + k] = sm[r * a.pitch + padi(j * N + m)];
       }
     } else {
       const int64_t base = ((int64_t)tb * a.P + p) * M;
-      for (int e = threadIdx.x; e < R * M; e += blockDim.x) {
-        const int i = e >> a.log2rows, r = e & (R - 1);
-        const float2 z = sm[r * a.pitch + i];
-        const int64_t o = (base + i) * a.tb + g0 + r;
+      for (int e = threadIdx.x; e < R * M; e += kFftThreads) {
+        const int k = e >> a.log2rows, r = e & (R - 1);
+        const int j = k & (a.os - 1), m = k >> a.log2os;
+        const float2 z = sm[r * a.pitch + padi(j * N + m)];
+        const int64_t o = (base + k) * a.tb + g0 + r;
         if (a.out_kind == FFT_GATHER_COMPLEX) {
           static_cast<float2*>(a.out)[o] = z;
         } else {
@@ -243,8 +365,8 @@ int ilog2(int v) {
 
 const float2* twiddles(Ctx* ctx, int M) {
   if (ctx->twiddle_m != M) {
-    std::vector<float2> h(static_cast<size_t>(M / 2));
-    for (int k = 0; k < M / 2; ++k) {
+    std::vector<float2> h(static_cast<size_t>(M));
+    for (int k = 0; k < M; ++k) {
       const double a = -2.0 * 3.141592653589793238462643383279502884 * k / M;
       h[static_cast<size_t>(k)] = make_float2((float)cos(a), (float)sin(a));
     }
@@ -264,7 +386,7 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   const int M = N * os;
   if ((N & (N - 1)) || (os & (os - 1)) || N < 2)
     fail(GH_EINVAL, "spectra: n_samples and os_range must be powers of two");
-  if (M > 65536) fail(GH_EINVAL, "spectra: FFT length above 65536 unsupported");
+  if (M > 16384) fail(GH_EINVAL, "spectra: FFT length above 16384 unsupported");
   if (tb < 1 || tb > 32 || (tb & (tb - 1))) fail(GH_EINVAL, "spectra: bad trial batch");
   FftArgs a{};
   a.frames = frames_d;
@@ -274,21 +396,33 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   a.P = P;
   a.N = N;
   a.M = M;
-  a.log2n = ilog2(N);
-  a.log2m = ilog2(M);
   a.os = os;
   a.log2os = ilog2(os);
+  a.log2n = ilog2(N);
   a.tb = tb;
-  // rows per pass: power of two <= min(tb, 16) within ~200 KB of smem
+  // rows per pass: two padded row buffers + the twiddle table in ~200 KB
   int R = tb < 16 ? tb : 16;
-  while (R > 1 && static_cast<size_t>(R) * (M + 16) * sizeof(float2) > 200 * 1024) R >>= 1;
+  const int pitch = M + M / 16 + 1;  // padded row, odd in float2 units
+  auto bytes = [&](int r) {
+    return (2 * static_cast<size_t>(r) * pitch + N) * sizeof(float2);
+  };
+  while (R > 1 && bytes(R) > 200 * 1024) R >>= 1;
+  if (bytes(R) > 220 * 1024) fail(GH_EINVAL, "spectra: FFT too long for one CTA");
   a.rows = R;
   a.log2rows = ilog2(R);
-  a.pitch = M + 16 / (R < 16 ? R : 16);
+  a.log2m = ilog2(M);
+  a.pitch = pitch;
+  // radix-16 passes, then one radix-8/4/2 pass for the remainder
+  a.npass = 0;
+  for (int rem = a.log2n; rem > 0;) {
+    const int lr = rem >= 4 ? 4 : rem;
+    a.pass_log2r[a.npass++] = lr;
+    rem -= lr;
+  }
   a.out_kind = out_kind;
   a.tw = twiddles(ctx, M);
   a.out = out_d;
-  const size_t smem = static_cast<size_t>(R) * a.pitch * sizeof(float2);
+  const size_t smem = bytes(R);
   GH_CUDA(cudaFuncSetAttribute(k_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const int n_tb = (T + tb - 1) / tb;

@@ -6,16 +6,23 @@
 // with Mc = 1, and argmax_index (src/direct.cpp:55-62, first strict max).
 //
 // One CTA = (trial batch of TB trials, location tile). It stages the tile's
-// per-pair range windows of the batch's spectra into shared memory (layout
-// [row][trial], one TB-run per row, so the TB lanes of a bin read one
-// contiguous, bank-conflict-free run), then every warp walks bins: lane t
-// of a TB-lane group accumulates trial t's value for one bin over all
-// pairs. The table (uint16 shared-memory rows, 4 pairs per 64-bit load) is
-// read once per batch of TB trials and broadcast within the lane group.
-// Argmax is fused: per-thread running max over its bins (increasing order,
-// strict >), merged across warps with the smallest-index tie rule, then one
-// 64-bit atomicMax per (CTA, trial) on key = float_bits(value) << 32 |
-// (2^32 - 1 - bin), which orders by value and then by smallest bin.
+// per-pair range windows of the batch's spectra into shared memory, layout
+// [row][trial]: one TB-run per FFT bin. Lanes are 16-byte vectors: a group
+// of L = TB*esize/16 lanes reads one row with LDS.128 (4 trials of power or
+// 2 trials of complex spectrum per lane), so a warp serves 32/L bins per
+// step; a 128-byte row (32 trials of power, 16 of complex) is exactly one
+// shared-memory wavefront, i.e. bank-conflict free.
+// The table holds, per (bin, pair), the uint16 shared-memory offset of the
+// bin's first row in 16-byte units (row * L), 4 pairs per 64-bit word. It
+// streams once per batch of TB trials: each warp owns a contiguous run of
+// bins, lane l loads the words of bin l of the next 32-bin block
+// (coalesced, one block ahead) and the words reach the lane groups by
+// shuffles. Accumulation uses sm_100's packed fp32 adds (FADD2 / FFMA2).
+// Argmax is fused: per-lane running max per trial over its bins (increasing
+// order, strict >), merged across warps with the smallest-index tie rule,
+// then one 64-bit atomicMax per (CTA, trial) on
+//   key = float_bits(value) << 32 | (2^32 - 1 - bin)
+// which orders by value, then by the smallest bin.
 #include <cuda_runtime.h>
 
 #include "gh_internal.cuh"
@@ -29,7 +36,7 @@ struct GatherArgs {
   const void* spec;       // [batches][P][M][TB] float or float2
   const TileDesc* tiles;  // tiled plan
   const int4* win;        // [tiles][P] / [P]
-  const uint16_t* rows;   // [entries][p4]
+  const uint16_t* rows;   // [entries][p4], 16-byte units
   const float2* coef3;    // [entries][P][3]
   gh_grid grid;
   int64_t G;
@@ -40,15 +47,66 @@ struct GatherArgs {
   unsigned long long* keys;
 };
 
-template <int TB, bool K3, bool MAG, bool MAPMODE>
+__device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDesc& td,
+                                              int64_t entry0, int64_t lb) {
+  if (a.full) return entry0 + lb;
+  const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
+  return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
+}
+
+__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
+
+// value contribution of one pair for the lane's trials
+template <int TB, bool K3, bool MAG, int L>
+__device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsigned off16,
+                                           const float2* __restrict__ cf, float2 (&acc)[2],
+                                           bool first) {
+  if constexpr (!K3) {
+    const float4 z = smv[off16];
+    if (first) {
+      acc[0] = f2(z.x, z.y);
+      acc[1] = f2(z.z, z.w);
+    } else {
+      acc[0] = __fadd2_rn(acc[0], f2(z.x, z.y));
+      acc[1] = __fadd2_rn(acc[1], f2(z.z, z.w));
+    }
+  } else {
+    const float2 c0 = __ldg(cf), c1 = __ldg(cf + 1), c2 = __ldg(cf + 2);
+    const float4 z0 = smv[off16];
+    const float4 z1 = smv[off16 + L];
+    const float4 z2 = smv[off16 + 2 * L];
+    // trial a = (x, y), trial b = (z, w); v = sum_j c_j z_j (complex product)
+    float2 ra = __fmul2_rn(f2(c0.x, c0.x), f2(z0.x, z0.y));           // (c0r*zr, c0r*zi)
+    ra = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.y, z0.x), ra);              // (-c0i*zi, c0i*zr)
+    ra = __ffma2_rn(f2(c1.x, c1.x), f2(z1.x, z1.y), ra);
+    ra = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.y, z1.x), ra);
+    ra = __ffma2_rn(f2(c2.x, c2.x), f2(z2.x, z2.y), ra);
+    ra = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.y, z2.x), ra);
+    float2 rb = __fmul2_rn(f2(c0.x, c0.x), f2(z0.z, z0.w));
+    rb = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.w, z0.z), rb);
+    rb = __ffma2_rn(f2(c1.x, c1.x), f2(z1.z, z1.w), rb);
+    rb = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.w, z1.z), rb);
+    rb = __ffma2_rn(f2(c2.x, c2.x), f2(z2.z, z2.w), rb);
+    rb = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.w, z2.z), rb);
+    const float2 sq = __ffma2_rn(f2(ra.x, rb.x), f2(ra.x, rb.x),
+                                 __fmul2_rn(f2(ra.y, rb.y), f2(ra.y, rb.y)));
+    const float2 v = MAG ? f2(sqrtf(sq.x), sqrtf(sq.y)) : sq;
+    if (first) acc[0] = v;
+    else acc[0] = __fadd2_rn(acc[0], v);
+  }
+}
+
+// PC: compile-time pair count (0 = runtime, at most 4 * PQ)
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
 __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
-  using E = typename std::conditional<K3, float2, float>::type;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  E* sm = reinterpret_cast<E*>(smraw);
-  constexpr int BPW = 32 / TB;  // bins per warp step
+  constexpr int ES = K3 ? 8 : 4;         // staged element bytes
+  constexpr int L = TB * ES / 16;        // lanes per row (16 B each)
+  constexpr int TPL = 16 / ES;           // trials per lane
+  constexpr int BPW = 32 / L;            // bins per warp step
   constexpr int NW = kGatherThreads / 32;
-  __shared__ float red_v[NW * BPW * TB];
-  __shared__ int red_i[NW * BPW * TB];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ float red_v[NW * TB];
+  __shared__ int red_i[NW * TB];
 
   const int tb = blockIdx.x;
   int64_t entry0, nb;
@@ -64,101 +122,145 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
     nb = (int64_t)td.wx * td.wy * td.wz;
     win = a.win + (int64_t)blockIdx.y * a.P;
   }
+  const int P = PC ? PC : a.P;
 
   // ---- stage the windows: rows (base + r) mod M of every pair
-  constexpr int CPR = TB * (int)sizeof(E) / 16;  // 16-byte chunks per row
-  const E* spec = static_cast<const E*>(a.spec) + (int64_t)tb * a.P * a.M * TB;
-  for (int p = 0; p < a.P; ++p) {
+  const uint4* spec = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(a.spec) +
+                                                     (int64_t)tb * a.P * a.M * TB * ES);
+  uint4* sm4 = reinterpret_cast<uint4*>(smraw);
+  for (int p = 0; p < P; ++p) {
     const int4 w = win[p];
-    const uint4* src = reinterpret_cast<const uint4*>(spec + (int64_t)p * a.M * TB);
-    uint4* dst = reinterpret_cast<uint4*>(sm + (int64_t)w.z * TB);
-    const int n = w.y * CPR;
+    const uint4* src = spec + (int64_t)p * a.M * L;
+    uint4* dst = sm4 + (int64_t)w.z * L;
+    const int n = w.y * L;
     for (int c = threadIdx.x; c < n; c += kGatherThreads) {
-      const int r = c / CPR, q = c - r * CPR;
+      const int r = c / L, q = c - r * L;
       int gi = w.x + r;
       while (gi >= a.M) gi -= a.M;
-      dst[c] = __ldg(src + (int64_t)gi * CPR + q);
+      dst[c] = __ldg(src + (int64_t)gi * L + q);
     }
   }
   __syncthreads();
 
   // ---- gather
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane / TB, t = lane % TB;
-  float best = -1.0f;
-  int blb = -1;
-  for (int64_t lb = warp * BPW + sub; lb < nb; lb += NW * BPW) {
-    const uint16_t* rw = a.rows + (entry0 + lb) * a.p4;
-    float acc = 0.0f;
-    for (int p0 = 0; p0 < a.P; p0 += 4) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(rw + p0));
-      const int rr[4] = {(int)(v.x & 0xffffu), (int)(v.x >> 16), (int)(v.y & 0xffffu),
-                         (int)(v.y >> 16)};
+  const int sub = lane / L, v = lane % L;
+  const float4* smv = reinterpret_cast<const float4*>(smraw) + v;  // this lane's column
+  float best[TPL];
+  int blb[TPL];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (p0 + q >= a.P) break;
-        if constexpr (!K3) {
-          acc += sm[rr[q] * TB + t];
+  for (int i = 0; i < TPL; ++i) {
+    best[i] = -1.0f;
+    blb[i] = -1;
+  }
+  const int64_t per_warp = ((nb + NW - 1) / NW + 31) / 32 * 32;
+  const int64_t w0 = warp * per_warp;
+  const int64_t w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
+  const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);  // uint2 words (4 pairs) per bin
+  const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
+  uint2 cur[PQ], nxt[PQ];
+#pragma unroll
+  for (int q = 0; q < PQ; ++q) {
+    cur[q] = make_uint2(0u, 0u);
+    nxt[q] = make_uint2(0u, 0u);
+  }
+  if (w0 + lane < w1)
+#pragma unroll
+    for (int q = 0; q < PQ; ++q)
+      if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
+  for (int64_t blk = w0; blk < w1; blk += 32) {
+    if (blk + 32 + lane < w1)
+#pragma unroll
+      for (int q = 0; q < PQ; ++q)
+        if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
+    const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
+#pragma unroll 2
+    for (int s = 0; s < 32 / BPW; ++s) {
+      if (s * BPW >= nblk) break;
+      const int j = s * BPW + sub;  // bin of this lane group within the block
+      const int64_t lb = blk + (j < nblk ? j : 0);
+      float2 acc[2];
+      acc[0] = acc[1] = f2(0.f, 0.f);
+      const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
+#pragma unroll
+      for (int q = 0; q < PQ; ++q) {
+        if (q >= pq) break;
+        const unsigned ex = __shfl_sync(0xffffffffu, cur[q].x, j & 31);
+        const unsigned ey = __shfl_sync(0xffffffffu, cur[q].y, j & 31);
+        const unsigned o[4] = {ex & 0xffffu, ex >> 16, ey & 0xffffu, ey >> 16};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = 4 * q + u;
+          if (PC ? p >= PC : p >= a.P) break;
+          accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p, acc, p == 0);
+        }
+      }
+      float vals[TPL];
+      if constexpr (!K3) {
+        vals[0] = acc[0].x;
+        vals[1] = acc[0].y;
+        vals[2 % TPL] = acc[1].x;
+        vals[3 % TPL] = acc[1].y;
+      } else {
+        vals[0] = acc[0].x;
+        vals[1] = acc[0].y;
+      }
+      if (j < nblk) {
+        if constexpr (MAPMODE) {
+          const int64_t gb = global_bin(a, td, entry0, lb);
+#pragma unroll
+          for (int i = 0; i < TPL; ++i) {
+            const int trial = tb * TB + v * TPL + i;
+            if (trial < a.T) a.map[(int64_t)trial * a.G + gb] = vals[i];
+          }
         } else {
-          const float2* cf = a.coef3 + ((entry0 + lb) * a.P + p0 + q) * 3;
-          const float2 c0 = __ldg(cf), c1 = __ldg(cf + 1), c2 = __ldg(cf + 2);
-          const float2 z0 = sm[rr[q] * TB + t];
-          const float2 z1 = sm[(rr[q] + 1) * TB + t];
-          const float2 z2 = sm[(rr[q] + 2) * TB + t];
-          const float vr = c0.x * z0.x - c0.y * z0.y + c1.x * z1.x - c1.y * z1.y +
-                           c2.x * z2.x - c2.y * z2.y;
-          const float vi = c0.x * z0.y + c0.y * z0.x + c1.x * z1.y + c1.y * z1.x +
-                           c2.x * z2.y + c2.y * z2.x;
-          const float pw = vr * vr + vi * vi;
-          acc += MAG ? sqrtf(pw) : pw;
+#pragma unroll
+          for (int i = 0; i < TPL; ++i)
+            if (vals[i] > best[i]) {
+              best[i] = vals[i];
+              blb[i] = (int)lb;
+            }
         }
       }
     }
-    if constexpr (MAPMODE) {
-      const int trial = tb * TB + t;
-      if (trial < a.T) {
-        int64_t gb = entry0 + lb;
-        if (!a.full) {
-          const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy,
-                        lz = lb / ((int64_t)td.wx * td.wy);
-          gb = (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
-        }
-        a.map[(int64_t)trial * a.G + gb] = acc;
-      }
-    } else {
-      if (acc > best) {
-        best = acc;
-        blb = (int)lb;
-      }
-    }
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
   }
   if constexpr (!MAPMODE) {
-    red_v[(warp * BPW + sub) * TB + t] = best;
-    red_i[(warp * BPW + sub) * TB + t] = blb;
+    // merge the BPW lane groups of the warp (same trials, different bins)
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) {
+      for (int o = L; o < 32; o <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best[i], o);
+        const int oi = __shfl_xor_sync(0xffffffffu, blb[i], o);
+        if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && oi < blb[i]))) {
+          best[i] = ov;
+          blb[i] = oi;
+        }
+      }
+      if (sub == 0) {
+        red_v[warp * TB + v * TPL + i] = best[i];
+        red_i[warp * TB + v * TPL + i] = blb[i];
+      }
+    }
     __syncthreads();
     if (threadIdx.x < TB) {
       float bv = -1.0f;
       int bi = -1;
-      for (int s = 0; s < NW * BPW; ++s) {
-        const float v = red_v[s * TB + threadIdx.x];
-        const int i = red_i[s * TB + threadIdx.x];
+      for (int w = 0; w < NW; ++w) {
+        const float val = red_v[w * TB + threadIdx.x];
+        const int i = red_i[w * TB + threadIdx.x];
         if (i < 0) continue;
-        if (v > bv || (v == bv && i < bi)) {
-          bv = v;
+        if (bi < 0 || val > bv || (val == bv && i < bi)) {
+          bv = val;
           bi = i;
         }
       }
       const int trial = tb * TB + threadIdx.x;
       if (trial < a.T && bi >= 0) {
-        int64_t gb = entry0 + bi;
-        if (!a.full) {
-          const int64_t lx = bi % td.wx, ly = (bi / td.wx) % td.wy,
-                        lz = bi / ((int64_t)td.wx * td.wy);
-          gb = (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
-        }
-        const unsigned long long key =
-            ((unsigned long long)__float_as_uint(bv) << 32) | (0xffffffffull - (unsigned long long)gb);
-        atomicMax(a.keys + trial, key);
+        const unsigned long long gb = (unsigned long long)global_bin(a, td, entry0, bi);
+        atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                      (0xffffffffull - gb));
       }
     }
   }
@@ -177,9 +279,9 @@ __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* id
   val[t] = __uint_as_float((unsigned)(k >> 32));
 }
 
-template <int TB, bool K3, bool MAG, bool MAPMODE>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
 void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_gather<TB, K3, MAG, MAPMODE>;
+  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   KTimer kt(ctx, "gather");
@@ -187,14 +289,28 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   GH_LAUNCHED(ctx);
 }
 
+// compile-time pair counts of the BASELINE configs (3, 16, 64), runtime
+// otherwise (PQ = uint2 words of 4 pairs per bin)
+template <int TB, bool K3, bool MAG, bool MAPMODE>
+void dispatch_p(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
+  const int pq = a.p4 / 4;
+  if (a.P == 3) run<TB, K3, MAG, MAPMODE, 3, 1>(ctx, a, grid, smem);
+  else if (a.P == 16) run<TB, K3, MAG, MAPMODE, 16, 4>(ctx, a, grid, smem);
+  else if (a.P == 64) run<TB, K3, MAG, MAPMODE, 64, 16>(ctx, a, grid, smem);
+  else if (pq <= 1) run<TB, K3, MAG, MAPMODE, 0, 1>(ctx, a, grid, smem);
+  else if (pq <= 4) run<TB, K3, MAG, MAPMODE, 0, 4>(ctx, a, grid, smem);
+  else if (pq <= 16) run<TB, K3, MAG, MAPMODE, 0, 16>(ctx, a, grid, smem);
+  else fail(GH_EINVAL, "gather: at most 64 TX-RX pairs");
+}
+
 template <int TB, bool K3>
 void dispatch(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem, bool mag, bool mapmode) {
   if (mapmode) {
-    if (mag) run<TB, K3, true, true>(ctx, a, grid, smem);
-    else run<TB, K3, false, true>(ctx, a, grid, smem);
+    if (mag) dispatch_p<TB, K3, true, true>(ctx, a, grid, smem);
+    else dispatch_p<TB, K3, false, true>(ctx, a, grid, smem);
   } else {
-    if (mag) run<TB, K3, true, false>(ctx, a, grid, smem);
-    else run<TB, K3, false, false>(ctx, a, grid, smem);
+    if (mag) dispatch_p<TB, K3, true, false>(ctx, a, grid, smem);
+    else dispatch_p<TB, K3, false, false>(ctx, a, grid, smem);
   }
 }
 

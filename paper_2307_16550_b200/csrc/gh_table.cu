@@ -303,7 +303,7 @@ struct FillArgs {
   const int4* win;        // [tiles][P] (full: [P])
   const uint32_t* idx;    // [G][P][K]
   const double2* coef;
-  int P, K, M, p4, k3;
+  int P, K, M, p4, k3, lanes;
   int64_t G;
   uint16_t* rows;
   float2* coef3;
@@ -334,7 +334,11 @@ __global__ void k_fill_plan(FillArgs a) {
     const int first = (int)a.idx[at];
     const int local = ((first - w.x) % a.M + a.M) % a.M;
     if (local + (a.k3 ? 2 : 0) >= w.y) atomicOr(a.err, 1);
-    a.rows[(entry0 + lb) * a.p4 + p] = (uint16_t)(w.z + local);
+    // stored in 16-byte units of the staged row layout (row * L), so the
+    // gather forms the shared-memory address with one shift-add
+    const int off16 = (w.z + local) * a.lanes;
+    if (off16 > 65535) atomicOr(a.err, 2);
+    a.rows[(entry0 + lb) * a.p4 + p] = (uint16_t)off16;
     if (a.k3) {
       float2* c3 = a.coef3 + ((entry0 + lb) * a.P + p) * 3;
       for (int j = 0; j < 3; ++j) {
@@ -581,6 +585,7 @@ void build_plan(Ctx* ctx, Table* t) {
   f.M = M;
   f.p4 = pl.p4;
   f.k3 = pl.k3;
+  f.lanes = pl.tb * pl.esize / 16;
   f.G = t->G;
   f.rows = pl.rows_d;
   f.coef3 = pl.coef3_d;
