@@ -162,47 +162,84 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-constexpr int brev_c(int i, int bits) {
-  int r = 0;
-  for (int b = 0; b < bits; ++b)
-    if (i & (1 << b)) r |= 1 << (bits - 1 - b);
-  return r;
-}
 constexpr int log2_c(int v) { return v <= 1 ? 0 : 1 + log2_c(v / 2); }
 
-// forward R-point DFT in registers (radix-2 DIT, constant twiddles)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+// x * W16^e (e a compile-time constant after unrolling)
+__device__ __forceinline__ float2 w16(float2 x, int e) {
+  e &= 15;
+  if (e == 0) return x;
+  if (e == 4) return make_float2(x.y, -x.x);   // * -i
+  if (e == 8) return make_float2(-x.x, -x.y);  // * -1
+  if (e == 12) return make_float2(-x.y, x.x);  // * +i
+  return cmul(x, make_float2(kC16[e], -kS16[e]));
+}
+
+// in-place forward 4-point DFT, natural order
+__device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d) {
+  const float2 t0 = cadd(a, c), t1 = csub(a, c);
+  const float2 t2 = cadd(b, d), u = csub(b, d);
+  const float2 t3 = make_float2(u.y, -u.x);  // (b - d) * -i
+  a = cadd(t0, t2);
+  c = csub(t0, t2);
+  b = cadd(t1, t3);
+  d = csub(t1, t3);
+}
+
+// Forward R-point DFT in registers, natural order in and out. Written as
+// explicit 4x4 / 2x4 factorisations with linear constant indices only: a
+// runtime-looking permutation index (bit reversal in a loop) would demote
+// v[] to local memory.
 template <int R>
 __device__ __forceinline__ void dft_reg(float2* v) {
-  constexpr int LB = log2_c(R);
+  if constexpr (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    dft4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    // n = 2 n1 + n2, k = k1 + 4 k2
+    float2 y[8];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int j = brev_c(i, LB);
-    if (j > i) {
-      const float2 t = v[i];
-      v[i] = v[j];
-      v[j] = t;
+    for (int n2 = 0; n2 < 2; ++n2) {
+      float2 a = v[n2], b = v[2 + n2], c = v[4 + n2], d = v[6 + n2];
+      dft4(a, b, c, d);
+      y[0 * 2 + n2] = a;
+      y[1 * 2 + n2] = w16(b, 2 * n2 * 1);
+      y[2 * 2 + n2] = w16(c, 2 * n2 * 2);
+      y[3 * 2 + n2] = w16(d, 2 * n2 * 3);
     }
-  }
 #pragma unroll
-  for (int len = 2; len <= R; len <<= 1) {
+    for (int k1 = 0; k1 < 4; ++k1) {
+      const float2 a = y[k1 * 2], b = y[k1 * 2 + 1];
+      v[k1] = cadd(a, b);
+      v[k1 + 4] = csub(a, b);
+    }
+  } else {
+    static_assert(R == 16, "radix 2, 4, 8 or 16");
+    // n = 4 n1 + n2, k = k1 + 4 k2
+    float2 y[16];
 #pragma unroll
-    for (int i = 0; i < R; i += len)
+    for (int n2 = 0; n2 < 4; ++n2) {
+      float2 a = v[n2], b = v[4 + n2], c = v[8 + n2], d = v[12 + n2];
+      dft4(a, b, c, d);
+      y[0 * 4 + n2] = a;
+      y[1 * 4 + n2] = w16(b, n2 * 1);
+      y[2 * 4 + n2] = w16(c, n2 * 2);
+      y[3 * 4 + n2] = w16(d, n2 * 3);
+    }
 #pragma unroll
-      for (int k = 0; k < len / 2; ++k) {
-        const int e = k * (16 / len);  // exp(-2 pi i k / len) = W16^e
-        const float2 b0 = v[i + k + len / 2];
-        float2 b;
-        if (e == 0) {
-          b = b0;
-        } else if (e == 4) {  // -i
-          b = make_float2(b0.y, -b0.x);
-        } else {
-          b = cmul(b0, make_float2(kC16[e], -kS16[e]));
-        }
-        const float2 a = v[i + k];
-        v[i + k] = make_float2(a.x + b.x, a.y + b.y);
-        v[i + k + len / 2] = make_float2(a.x - b.x, a.y - b.y);
-      }
+    for (int k1 = 0; k1 < 4; ++k1) {
+      float2 a = y[k1 * 4 + 0], b = y[k1 * 4 + 1], c = y[k1 * 4 + 2], d = y[k1 * 4 + 3];
+      dft4(a, b, c, d);
+      v[k1] = a;
+      v[k1 + 4] = b;
+      v[k1 + 8] = c;
+      v[k1 + 12] = d;
+    }
   }
 }
 
@@ -357,10 +394,218 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft(FftArgs a) {
   }
 }
 
+// ------------------------------------------------------------ fixed-size FFT
+// The same algorithm with N, os and the rows per pass as compile-time
+// constants (the BASELINE sizes): every shared-memory offset folds into an
+// immediate, which removes the index arithmetic that dominates the generic
+// kernel's instruction count.
+__host__ __device__ constexpr int pad_c(int i) { return i + (i >> 4); }
+
+constexpr int kFxThreads = 256;
+
+template <int LN, int LOS, int LROWS>
+struct Fx {
+  static constexpr int N = 1 << LN, OS = 1 << LOS, M = N * OS, ROWS = 1 << LROWS;
+  // padded sub-FFT stride, odd so the os sub-rows of one bin hit distinct banks
+  static constexpr int SUBP = N + N / 16 + 1;
+  static constexpr int PITCH = OS * SUBP + ((OS * SUBP) % 2 == 0 ? 1 : 0);
+  static constexpr int NP = (LN + 3) / 4;
+  static constexpr int lr(int ps) { return LN - 4 * ps >= 4 ? 4 : LN - 4 * ps; }
+  static constexpr size_t smem_bytes() { return (2ull * ROWS * PITCH + N) * 8; }
+  static_assert(LN >= 4, "fixed FFT needs N >= 16");
+};
+
+template <int LN, int LOS, int LROWS, int PS>
+__device__ __forceinline__ void fixed_pass(const float2* __restrict__ src, float2* __restrict__ dst,
+                                           const float2* __restrict__ ptw) {
+  using F = Fx<LN, LOS, LROWS>;
+  constexpr int LRR = F::lr(PS), R = 1 << LRR, NS = 1 << (4 * PS);
+  constexpr int PER = F::N / R;
+  constexpr int TASKS = F::ROWS * F::OS * PER;
+  constexpr int TW0 = (1 << (4 * PS)) - 1;  // sum of previous radix-16 tables
+#pragma unroll
+  for (int it = 0; it < (TASKS + kFxThreads - 1) / kFxThreads; ++it) {
+    const int task = threadIdx.x + it * kFxThreads;
+    if (TASKS % kFxThreads != 0 && task >= TASKS) break;
+    const int ro = task / PER, q = task % PER;
+    const int row = ro >> LOS, sub = ro & (F::OS - 1);
+    const int sbase = row * F::PITCH + sub * F::SUBP;
+    const int k = q & (NS - 1);
+    float2 v[R];
+    if constexpr (PER % 16 == 0) {
+      const float2* s = src + sbase + pad_c(q);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = s[r * (PER + PER / 16)];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = src[sbase + pad_c(q + r * PER)];
+    }
+    if constexpr (PS > 0) {
+      const float2* t = ptw + TW0 + k * (R - 1);
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], t[r - 1]);
+    }
+    dft_reg<R>(v);
+    const int o = (q - k) * R + k;
+    if constexpr (NS % 16 == 0) {
+      float2* d = dst + sbase + pad_c(o);
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[r * (NS + NS / 16)] = v[r];
+    } else {
+      // first pass: o = q * R is a multiple of 16 and r < 16
+      float2* d = dst + sbase + pad_c(o);
+#pragma unroll
+      for (int r = 0; r < R; ++r) d[r] = v[r];
+    }
+  }
+  __syncthreads();
+}
+
+template <int LN, int LOS, int LROWS, int PS>
+__device__ __forceinline__ float2* fixed_passes(float2* src, float2* dst, const float2* ptw) {
+  using F = Fx<LN, LOS, LROWS>;
+  if constexpr (PS < F::NP) {
+    fixed_pass<LN, LOS, LROWS, PS>(src, dst, ptw);
+    return fixed_passes<LN, LOS, LROWS, PS + 1>(dst, src, ptw);
+  } else {
+    return src;
+  }
+}
+
+template <int LN, int LOS, int LROWS>
+__global__ void __launch_bounds__(kFxThreads) k_fft_fixed(FftArgs a) {
+  using F = Fx<LN, LOS, LROWS>;
+  constexpr int N = F::N, M = F::M, R = F::ROWS;
+  extern __shared__ float2 smem_dyn[];
+  __shared__ RowSynth rsm[16];
+  float2* ptw = smem_dyn;
+  float2* buf0 = smem_dyn + N;
+  float2* buf1 = buf0 + R * F::PITCH;
+  const int tb = blockIdx.x, p = blockIdx.y;
+  const double inv_n = 1.0 / (double)N;
+  {
+    int toff = 0;
+#pragma unroll
+    for (int ps = 1; ps < F::NP; ++ps) {
+      const int lr = F::lr(ps), rp = 1 << lr, lns = 4 * ps, ns = 1 << lns;
+      toff = (1 << lns) - 1;
+      const int cnt = ns * (rp - 1);
+      const int step = LN + LOS - lns - lr;
+      for (int e = threadIdx.x; e < cnt; e += kFxThreads) {
+        const int k = e / (rp - 1), r = e - k * (rp - 1) + 1;
+        ptw[toff + e] = __ldg(a.tw + ((r * k) << step));
+      }
+    }
+  }
+  for (int g0 = 0; g0 < a.tb; g0 += R) {
+    if (a.synth && threadIdx.x < R) {
+      const int t = tb * a.tb + g0 + threadIdx.x;
+      if (t < a.T) {
+        row_setup(a.sp, a.P, p, a.sp.trial0 + (uint64_t)t, rsm[threadIdx.x], a.sp.err_flag_d);
+        if (!a.sp.wrap)
+          for (int k = 0; k < a.sp.camp.n_targets; ++k) {
+            const double r = rsm[threadIdx.x].r[k];
+            if (!(r >= 0.0 && r < (double)N)) atomicOr(a.sp.err_flag_d, 1);
+          }
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int e = threadIdx.x; e < R * N; e += kFxThreads) {
+      const int r = e >> LN;
+      const int n = e & (N - 1);
+      const int t = tb * a.tb + g0 + r;
+      float2 v = make_float2(0.f, 0.f);
+      if (t < a.T) {
+        if (a.synth)
+          v = synth_sample(rsm[r], a.sp.camp.n_targets, n, inv_n);
+        else
+          v = a.frames[((int64_t)t * a.P + p) * N + n];
+      }
+      float2* row = buf0 + r * F::PITCH + pad_c(n);
+      row[0] = v;
+#pragma unroll
+      for (int j = 1; j < F::OS; ++j) row[j * F::SUBP] = cmul(v, __ldg(a.tw + j * n));
+    }
+    __syncthreads();
+    const float2* sm = fixed_passes<LN, LOS, LROWS, 0>(buf0, buf1, ptw);
+    if (a.out_kind == FFT_NATURAL) {
+      float2* out = static_cast<float2*>(a.out);
+      for (int e = threadIdx.x; e < R * M; e += kFxThreads) {
+        const int r = e / M, k = e % M;
+        const int t = tb * a.tb + g0 + r;
+        const int j = k & (F::OS - 1), m = k >> LOS;
+        if (t < a.T) out[((int64_t)t * a.P + p) * M + k] = sm[r * F::PITCH + j * F::SUBP + pad_c(m)];
+      }
+    } else {
+      // one thread per range bin k: the R rows' values are contiguous in the
+      // gather layout [batch][pair][k][TB] -> vector stores
+      const int64_t base = ((int64_t)tb * a.P + p) * M;
+#pragma unroll 2
+      for (int k = threadIdx.x; k < M; k += kFxThreads) {
+        const int j = k & (F::OS - 1), m = k >> LOS;
+        const float2* s = sm + j * F::SUBP + pad_c(m);
+        float2 z[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) z[r] = s[r * F::PITCH];
+        const int64_t o = (base + k) * a.tb + g0;
+        if (a.out_kind == FFT_GATHER_COMPLEX) {
+          float2* dst = static_cast<float2*>(a.out) + o;
+          if constexpr (R % 2 == 0) {
+#pragma unroll
+            for (int r = 0; r < R; r += 2)
+              *reinterpret_cast<float4*>(dst + r) = make_float4(z[r].x, z[r].y, z[r + 1].x, z[r + 1].y);
+          } else {
+            dst[0] = z[0];
+          }
+        } else {
+          float w[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const float pw = z[r].x * z[r].x + z[r].y * z[r].y;
+            w[r] = (a.out_kind == FFT_GATHER_MAG) ? sqrtf(pw) : pw;
+          }
+          float* dst = static_cast<float*>(a.out) + o;
+          if constexpr (R % 4 == 0) {
+#pragma unroll
+            for (int r = 0; r < R; r += 4)
+              *reinterpret_cast<float4*>(dst + r) = make_float4(w[r], w[r + 1], w[r + 2], w[r + 3]);
+          } else if constexpr (R == 2) {
+            *reinterpret_cast<float2*>(dst) = make_float2(w[0], w[1]);
+          } else {
+            dst[0] = w[0];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 int ilog2(int v) {
   int l = 0;
   while ((1 << l) < v) ++l;
   return l;
+}
+
+using FftKernel = void (*)(FftArgs);
+
+// compile-time instantiations: (log2 N, log2 os, log2 rows per pass); rows *
+// M = 4096 points per pass keeps a CTA near 70 KB (three CTAs per SM)
+FftKernel fixed_kernel(int ln, int los, int lrows, size_t* smem) {
+#define GH_FX(a, b, c)                              \
+  if (ln == a && los == b && lrows == c) {          \
+    *smem = Fx<a, b, c>::smem_bytes();              \
+    return k_fft_fixed<a, b, c>;                    \
+  }
+  GH_FX(6, 2, 4)   // N=64,   M=256  (small test scenes)
+  GH_FX(7, 0, 4)   // N=128,  M=128
+  GH_FX(8, 2, 2)   // N=256,  M=1024 (c1, c2)
+  GH_FX(9, 1, 2)   // N=512,  M=1024 (c4)
+  GH_FX(9, 2, 1)   // N=512,  M=2048 (c5)
+  GH_FX(10, 2, 0)  // N=1024, M=4096 (c3)
+#undef GH_FX
+  return nullptr;
 }
 
 const float2* twiddles(Ctx* ctx, int M) {
@@ -422,13 +667,27 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   a.out_kind = out_kind;
   a.tw = twiddles(ctx, M);
   a.out = out_d;
-  const size_t smem = bytes(R);
-  GH_CUDA(cudaFuncSetAttribute(k_fft, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  size_t smem = bytes(R);
+  int threads = kFftThreads;
+  // fixed-size kernel when this (N, os) has one: rows * M = 4096
+  int fr = 1;
+  while (fr * 2 <= (tb < 16 ? tb : 16) && fr * 2 * M <= 4096) fr *= 2;
+  size_t fsmem = 0;
+  FftKernel kern = fixed_kernel(a.log2n, a.log2os, ilog2(fr), &fsmem);
+  if (kern) {
+    a.rows = fr;
+    a.log2rows = ilog2(fr);
+    smem = fsmem;
+    threads = kFxThreads;
+  } else {
+    kern = k_fft;
+  }
+  GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   const int n_tb = (T + tb - 1) / tb;
   dim3 grid(n_tb, P);
   KTimer kt(ctx, synth ? "synth_fft" : "fft");
-  k_fft<<<grid, kFftThreads, smem, ctx->stream>>>(a);
+  kern<<<grid, threads, smem, ctx->stream>>>(a);
   GH_LAUNCHED(ctx);
 }
 

@@ -174,11 +174,10 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
       for (int q = 0; q < PQ; ++q)
         if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
-#pragma unroll 2
-    for (int s = 0; s < 32 / BPW; ++s) {
-      if (s * BPW >= nblk) break;
-      const int j = s * BPW + sub;  // bin of this lane group within the block
-      const int64_t lb = blk + (j < nblk ? j : 0);
+    // one step: lane group `sub` handles bin j = s * BPW + sub of the block
+    auto step = [&](int s, bool check) {
+      const int j = s * BPW + sub;
+      const int64_t lb = blk + (!check || j < nblk ? j : 0);
       float2 acc[2];
       acc[0] = acc[1] = f2(0.f, 0.f);
       const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
@@ -205,7 +204,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
         vals[0] = acc[0].x;
         vals[1] = acc[0].y;
       }
-      if (j < nblk) {
+      if (!check || j < nblk) {
         if constexpr (MAPMODE) {
           const int64_t gb = global_bin(a, td, entry0, lb);
 #pragma unroll
@@ -222,6 +221,18 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
             }
         }
       }
+    };
+    constexpr bool kUnroll = !K3 && PC > 0 && PC <= 16;
+    if (nblk == 32 && kUnroll) {
+      // full block: fixed trip count, no bounds checks, fully unrolled so
+      // the next step's shuffles and loads overlap this step's updates
+#pragma unroll
+      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
+    } else if (nblk == 32) {
+#pragma unroll 1
+      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
+    } else {
+      for (int s = 0; s * BPW < nblk; ++s) step(s, true);
     }
 #pragma unroll
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
