@@ -1,0 +1,92 @@
+"""Multi-GPU host logic: one process per GPU, torch.distributed for plumbing.
+
+The hot path shards two ways:
+  * trials: rank r owns a contiguous block of Monte-Carlo trials and
+    synthesises them from (seed, trial) counters — no signal traffic; the
+    only collective is one all-reduce(SUM) of a small statistics vector per
+    campaign cell (hit_ratio / RMSE, src/montecarlo.cpp:181-216);
+  * location grid (c5): every rank synthesises the same trials and scans its
+    own slab of the grid; per-trial candidates merge with one
+    all-reduce(MAX) of the 64-bit key  float_bits(value) << 32 | (2^32-1-bin),
+    which orders by value then smallest bin (argmax_index tie rule,
+    src/direct.cpp:55-62). Non-negative float bits keep the key below 2^63,
+    so it travels as int64.
+The same code runs over NCCL on GPUs and over gloo in the CPU tests.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+STATS_FIELDS = ("count", "hits_1m", "sq_err_sum", "hits_half_res")
+
+
+def shard(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous [lo, hi) block of n items for rank (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def grid_slab(nz: int, ny: int, world: int, rank: int) -> tuple[int, int]:
+    """Location-grid sharding: rank's [z0, z1) slab (or y rows for 2-D)."""
+    return shard(nz if nz > 1 else ny, world, rank)
+
+
+def campaign_stats(scene, est_idx: np.ndarray, truth: np.ndarray, threshold_m: float = 1.0) -> np.ndarray:
+    """[count, hits within threshold, sum of squared location error, hits
+    within half a range resolution] for single-target trials (truth [T, K, 3],
+    target 0). Location of the estimate = its grid point."""
+    est = scene.grid_points(est_idx)
+    err = np.linalg.norm(est - truth[:, 0, :], axis=-1)
+    half_res = 0.5 * scene.c / (2 * scene.bandwidth)
+    return np.array([float(len(err)), float(np.sum(err <= threshold_m)), float(np.sum(err * err)),
+                     float(np.sum(err <= half_res))])
+
+
+def summarize(stats: np.ndarray) -> dict:
+    count = max(stats[0], 1.0)
+    return {"trials": int(stats[0]), "hit_ratio_1m": stats[1] / count,
+            "rmse_m": float(np.sqrt(stats[2] / count)), "hit_ratio_half_res": stats[3] / count}
+
+
+def allreduce_stats(stats: np.ndarray, device=None) -> np.ndarray:
+    """SUM over ranks (NCCL on GPU tensors, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(stats, dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().numpy()
+
+
+def encode_keys(values: np.ndarray, bins: np.ndarray) -> np.ndarray:
+    """Per-trial (value >= 0, global bin) -> int64 key, max == argmax rule."""
+    vb = np.asarray(values, dtype=np.float32).view(np.uint32).astype(np.int64)
+    return (vb << 32) | (0xFFFFFFFF - np.asarray(bins, dtype=np.int64))
+
+
+def decode_keys(keys: np.ndarray):
+    keys = np.asarray(keys, dtype=np.int64)
+    bins = 0xFFFFFFFF - (keys & 0xFFFFFFFF)
+    vals = (keys >> 32).astype(np.uint32).view(np.float32)
+    return bins, vals
+
+
+def allreduce_argmax(values: np.ndarray, bins: np.ndarray, device=None):
+    """Merge per-rank shard winners into the global per-trial argmax."""
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(encode_keys(values, bins)).to(device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return decode_keys(t.cpu().numpy())
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Step time of a multi-rank run: the slowest rank (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
