@@ -74,6 +74,7 @@ def lib() -> C.CDLL:
             "gh_ctx_kernel_time": (C.c_int, [vp, C.c_char_p, P(f64), P(i64)]),
             "gh_ctx_reset_timing": (C.c_int, [vp]),
             "gh_measure_smem_peak": (C.c_int, [vp, P(f64)]),
+            "gh_ctx_set_direct_impl": (C.c_int, [vp, i32]),
             "gh_table_build": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, P(vp)]),
             "gh_table_upload": (C.c_int, [vp, P(CWave), P(CGrid), i32, vp, vp, P(vp)]),
             "gh_table_info": (C.c_int, [vp, P(i64), P(i32), P(i32), P(i32), P(f64)]),
@@ -166,6 +167,10 @@ class Context:
 
     def reset_timing(self) -> None:
         _check(lib().gh_ctx_reset_timing(self.h))
+
+    def set_direct_impl(self, impl: str) -> None:
+        """'tcgen05' (default, 3xTF32 tensor cores) or 'simt' (CUDA-core fp32)."""
+        _check(lib().gh_ctx_set_direct_impl(self.h, {"tcgen05": 0, "simt": 1}[impl]))
 
     def smem_peak_gbps(self) -> float:
         v = C.c_double()

@@ -251,6 +251,15 @@ int gh_ctx_launch_count(gh_ctx* ctx, int64_t* count) {
   });
 }
 
+int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    if (impl != 0 && impl != 1) fail(GH_EINVAL, "ctx: direct impl must be 0 (tcgen05) or 1 (simt)");
+    c->direct_impl = impl;
+  });
+}
+
 int gh_ctx_set_timing(gh_ctx* ctx, int32_t on) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
@@ -522,7 +531,7 @@ int gh_direct_map_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const
     use_device(c);
     gh::Buffer txrx;
     const double* tr = upload_txrx(c, wave, txrx);
-    gh::direct_map_simt(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
+    gh::direct_map(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
                         combine, map_d, nullptr);
     GH_CUDA(cudaStreamSynchronize(c->stream));
     txrx.release();
@@ -546,7 +555,7 @@ int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
     const double* tr = upload_txrx(c, wave, txrx);
     auto* keys = static_cast<unsigned long long*>(c->keys.get(sizeof(unsigned long long) * n_trials));
     GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * n_trials, c->stream));
-    gh::direct_map_simt(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
+    gh::direct_map(c, tr, wave, grid, reinterpret_cast<const float2*>(frames_d), n_trials,
                         combine, nullptr, keys);
     gh::launch_decode_keys(c, keys, n_trials, idx_d, val_d);
     GH_CUDA(cudaStreamSynchronize(c->stream));

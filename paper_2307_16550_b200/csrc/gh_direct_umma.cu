@@ -1,0 +1,334 @@
+// gh_direct_umma.cu — the direct method on the 5th-generation tensor cores
+// (tcgen05 / TMEM, sm_100a), 3xTF32.
+//
+// Reference: location_decision_map (src/direct.cpp:90-144), Mc = 1:
+//   value(t, g) = sum_p | sum_n y_p[t, n] conj(a_n(r_p(g))) |^2
+// As a real contraction over K = 2N with k = 2n + c (c = 0 real, 1 imag —
+// the interleaved complex64 layout of the frames, so A rows are the frames
+// as stored):
+//   zr = sum_n yr cos + yi sin      -> B_re[2n] = cos, B_re[2n+1] = sin
+//   zi = sum_n yi cos - yr sin      -> B_im[2n] = -sin, B_im[2n+1] = cos
+// with cos/sin of 2 pi frac(r n / N) (phase reduced in fp64).
+//
+// CTA tile: 128 trials (MMA M, TMEM lanes) x 64 bins (MMA N = 128 columns:
+// 64 real + 64 imaginary parts). Per pair and K-chunk of 32, the CTA writes
+// A (frames) and B (steering, generated on the fly) into shared memory as
+// tf32 big/small halves (x = big + small, big = cvt.rna.tf32(x)), and one
+// thread issues 3 x 4 tcgen05.mma.kind::tf32 (big*big + big*small +
+// small*big: fp32-grade products) accumulating in TMEM. After each pair the
+// 4 epilogue warps read the accumulator with tcgen05.ld, add |z|^2 into
+// per-thread running sums, and after the last pair write the map or fold a
+// per-trial argmax into the 64-bit keys shared with the gather.
+//
+// Operand layout (canonical K-major, no swizzle): core matrices of 8 rows x
+// 16 bytes, stored [k-chunk of 16 B][row group of 8][row][16 B], so
+// SBO = 128 B (row groups) and LBO = rows/8 * 128 B (k-chunks).
+#include <cuda_runtime.h>
+
+#include "gh_internal.cuh"
+
+namespace gh {
+namespace {
+
+constexpr int BT = 128;      // trials per CTA (MMA M)
+constexpr int BGU = 64;      // bins per CTA (MMA N = 2 * BGU)
+constexpr int NCOL = 2 * BGU;
+constexpr int BK = 32;       // tf32 K elements per stage
+constexpr int KCH = BK / 4;  // 16-byte k-chunks per stage
+constexpr int kThreads = 256;
+constexpr int kMaxPairs = 64;
+
+// operand tile: rows x BK tf32, canonical K-major
+constexpr int TILE_BYTES_A = BT * BK * 4;    // 16 KB
+constexpr int TILE_BYTES_B = NCOL * BK * 4;  // 16 KB
+constexpr int LBO_A = BT / 8 * 128;
+constexpr int LBO_B = NCOL / 8 * 128;
+
+struct UmmaArgs {
+  const float2* frames;  // [T][P][N]
+  const double* txrx;    // [P][6]
+  gh_grid grid;
+  double scale;
+  int T, P, N;
+  int64_t G;
+  int mag;
+  float* map;
+  unsigned long long* keys;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// canonical K-major byte offset of (row, 16-byte k-chunk)
+__device__ __forceinline__ int kmaj_off(int row, int kc, int lbo) {
+  return kc * lbo + (row >> 3) * 128 + (row & 7) * 16;
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, SWIZZLE_NONE
+}
+
+// kind::tf32, fp32 accumulate, K-major A and B, M = 128, N = NCOL
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NCOL >> 3) << 17) |
+                            ((uint32_t)(BT >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_direct_umma(UmmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* a_big = sm;
+  unsigned char* a_sml = a_big + TILE_BYTES_A;
+  unsigned char* b_big = a_sml + TILE_BYTES_A;
+  unsigned char* b_sml = b_big + TILE_BYTES_B;
+  __shared__ double rho[BGU];  // r / N of the current pair: turns per sample
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * BT;
+  const int64_t g0 = (int64_t)blockIdx.y * BGU;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(NCOL));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const double inv_n = 1.0 / (double)a.N;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  float pw[BGU];  // running sum over pairs (epilogue warps 0-3: trial row)
+#pragma unroll
+  for (int j = 0; j < BGU; ++j) pw[j] = 0.f;
+
+  uint32_t phase = 0;
+  const int K2 = 2 * a.N;  // real K
+  for (int p = 0; p < a.P; ++p) {
+    if (threadIdx.x < BGU) {
+      const int64_t g = g0 + threadIdx.x;
+      double r = 0.0;
+      if (g < a.G) {
+        double x[3];
+        dgrid_point(a.grid, g, x);
+        const double* tp = a.txrx + 6 * p;
+        r = __dmul_rn(a.scale,
+                      __dadd_rn(dnorm3(tp, x[0], x[1], x[2]), dnorm3(tp + 3, x[0], x[1], x[2])));
+      }
+      rho[threadIdx.x] = r * inv_n;
+    }
+    __syncthreads();
+    for (int k0 = 0; k0 < K2; k0 += BK) {
+      // ---- A: 128 trials x 32 tf32 = 8 chunks of (2 complex samples)
+      for (int e = threadIdx.x; e < BT * KCH; e += kThreads) {
+        const int row = e / KCH, kc = e % KCH;
+        const int t = t0 + row;
+        const int n = (k0 >> 1) + 2 * kc;  // first complex sample of the chunk
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < a.T && n < a.N) {
+          const float4* src = reinterpret_cast<const float4*>(a.frames + ((int64_t)t * a.P + p) * a.N + n);
+          v = __ldg(src);
+        }
+        uint4 big, sml;
+        big.x = tf32_rna(v.x); sml.x = __float_as_uint(v.x - __uint_as_float(big.x));
+        big.y = tf32_rna(v.y); sml.y = __float_as_uint(v.y - __uint_as_float(big.y));
+        big.z = tf32_rna(v.z); sml.z = __float_as_uint(v.z - __uint_as_float(big.z));
+        big.w = tf32_rna(v.w); sml.w = __float_as_uint(v.w - __uint_as_float(big.w));
+        const int off = kmaj_off(row, kc, LBO_A);
+        *reinterpret_cast<uint4*>(a_big + off) = big;
+        *reinterpret_cast<uint4*>(a_sml + off) = sml;
+      }
+      // ---- B: 64 bins x 8 chunks; chunk = samples (n, n+1):
+      //      re column: (cos n, sin n, cos n+1, sin n+1)
+      //      im column: (-sin n, cos n, -sin n+1, cos n+1)
+      for (int e = threadIdx.x; e < BGU * KCH; e += kThreads) {
+        const int j = e / KCH, kc = e % KCH;
+        const int n = (k0 >> 1) + 2 * kc;
+        float c0 = 0.f, s0 = 0.f, c1 = 0.f, s1 = 0.f;
+        const double rj = rho[j];
+        if (n < a.N) {
+          const double ph0 = rj * (double)n, ph1 = rj * (double)(n + 1);
+          sincospif((float)(2.0 * (ph0 - floor(ph0))), &s0, &c0);
+          if (n + 1 < a.N) sincospif((float)(2.0 * (ph1 - floor(ph1))), &s1, &c1);
+        }
+        const float re[4] = {c0, s0, c1, s1};
+        const float im[4] = {-s0, c0, -s1, c1};
+        uint4 rb, rs, ib, is;
+        rb.x = tf32_rna(re[0]); rs.x = __float_as_uint(re[0] - __uint_as_float(rb.x));
+        rb.y = tf32_rna(re[1]); rs.y = __float_as_uint(re[1] - __uint_as_float(rb.y));
+        rb.z = tf32_rna(re[2]); rs.z = __float_as_uint(re[2] - __uint_as_float(rb.z));
+        rb.w = tf32_rna(re[3]); rs.w = __float_as_uint(re[3] - __uint_as_float(rb.w));
+        ib.x = tf32_rna(im[0]); is.x = __float_as_uint(im[0] - __uint_as_float(ib.x));
+        ib.y = tf32_rna(im[1]); is.y = __float_as_uint(im[1] - __uint_as_float(ib.y));
+        ib.z = tf32_rna(im[2]); is.z = __float_as_uint(im[2] - __uint_as_float(ib.z));
+        ib.w = tf32_rna(im[3]); is.w = __float_as_uint(im[3] - __uint_as_float(ib.w));
+        const int ore = kmaj_off(j, kc, LBO_B), oim = kmaj_off(BGU + j, kc, LBO_B);
+        *reinterpret_cast<uint4*>(b_big + ore) = rb;
+        *reinterpret_cast<uint4*>(b_sml + ore) = rs;
+        *reinterpret_cast<uint4*>(b_big + oim) = ib;
+        *reinterpret_cast<uint4*>(b_sml + oim) = is;
+      }
+      // generic-proxy writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t ab = smem_u32(a_big), as_ = smem_u32(a_sml);
+        const uint32_t bb = smem_u32(b_big), bs = smem_u32(b_sml);
+#pragma unroll
+        for (int s = 0; s < BK / 8; ++s) {
+          const uint64_t dab = umma_desc(ab + 2 * s * LBO_A, LBO_A, 128);
+          const uint64_t das = umma_desc(as_ + 2 * s * LBO_A, LBO_A, 128);
+          const uint64_t dbb = umma_desc(bb + 2 * s * LBO_B, LBO_B, 128);
+          const uint64_t dbs = umma_desc(bs + 2 * s * LBO_B, LBO_B, 128);
+          const uint32_t acc0 = (k0 > 0 || s > 0) ? 1u : 0u;
+          mma_tf32(tmem, dab, dbb, acc0);
+          mma_tf32(tmem, dab, dbs, 1u);
+          mma_tf32(tmem, das, dbb, 1u);
+        }
+        mma_commit(&mbar);
+      }
+      // operands are reused next chunk: wait for the MMAs to finish reading
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    // ---- epilogue for pair p: |z|^2 accumulated per (trial, bin)
+    if (warp < 4) {
+      const uint32_t row_addr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < BGU; c += 16) {
+        float re[16], im[16];
+        tmem_ld16(row_addr + c, re);
+        tmem_ld16(row_addr + BGU + c, im);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float q = re[i] * re[i] + im[i] * im[i];
+          pw[c + i] += a.mag ? sqrtf(q) : q;
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // TMEM drained before the next pair overwrites it
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+
+  if (warp < 4) {
+    const int t = t0 + warp * 32 + lane;
+    if (t < a.T) {
+      if (a.map) {
+        for (int j = 0; j < BGU; ++j)
+          if (g0 + j < a.G) a.map[(int64_t)t * a.G + g0 + j] = pw[j];
+      } else {
+        float bv = -1.f;
+        int bj = -1;
+#pragma unroll
+        for (int j = 0; j < BGU; ++j)
+          if (g0 + j < a.G && pw[j] > bv) {
+            bv = pw[j];
+            bj = j;
+          }
+        if (bj >= 0)
+          atomicMax(a.keys + t, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                    (0xffffffffull - (unsigned long long)(g0 + bj)));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NCOL));
+  }
+}
+
+}  // namespace
+
+void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                     const float2* frames_d, int T, int combine, float* map_d,
+                     unsigned long long* keys_d) {
+  UmmaArgs a{};
+  a.frames = frames_d;
+  a.txrx = txrx_d;
+  a.grid = *g;
+  a.scale = w->range_scale;
+  a.T = T;
+  a.P = w->n_pairs;
+  a.N = w->n_samples;
+  a.G = (int64_t)g->n[0] * g->n[1] * g->n[2];
+  a.mag = combine == GH_MAGNITUDE;
+  a.map = map_d;
+  a.keys = keys_d;
+  if (a.P > kMaxPairs) fail(GH_EINVAL, "direct: at most 64 TX-RX pairs");
+  if (a.N % 2) fail(GH_EINVAL, "direct: n_samples must be even");
+  const int64_t gb = (a.G + BGU - 1) / BGU;
+  if (gb > 65535) fail(GH_EINVAL, "direct: grid too large for one launch");
+  const size_t smem = 2 * TILE_BYTES_A + 2 * TILE_BYTES_B;
+  GH_CUDA(cudaFuncSetAttribute(k_direct_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  dim3 grid((T + BT - 1) / BT, static_cast<unsigned>(gb));
+  KTimer kt(ctx, "direct_umma");
+  k_direct_umma<<<grid, kThreads, smem, ctx->stream>>>(a);
+  GH_LAUNCHED(ctx);
+}
+
+}  // namespace gh

@@ -63,6 +63,7 @@ struct Ctx {
   size_t smem_optin = 227 * 1024;
   Buffer spectra, frames, keys, misc, twiddle_buf;
   int twiddle_m = 0;
+  int direct_impl = 0;  // 0: tcgen05 3xTF32, 1: CUDA-core fp32 (reference path)
   // optional per-kernel CUDA-event timing on the context stream
   bool timing = false;
   struct Pending {
@@ -210,5 +211,16 @@ void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
 void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const float2* frames_d, int T, int combine, float* map_d,
                      unsigned long long* keys_d);
+void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                     const float2* frames_d, int T, int combine, float* map_d,
+                     unsigned long long* keys_d);
+inline void direct_map(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                       const float2* frames_d, int T, int combine, float* map_d,
+                       unsigned long long* keys_d) {
+  if (ctx->direct_impl == 1)
+    direct_map_simt(ctx, txrx_d, w, g, frames_d, T, combine, map_d, keys_d);
+  else
+    direct_map_umma(ctx, txrx_d, w, g, frames_d, T, combine, map_d, keys_d);
+}
 
 }  // namespace gh

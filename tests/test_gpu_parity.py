@@ -156,17 +156,41 @@ def test_campaign_matches_oracle_campaign(ctx):
     assert np.allclose(g_val.cpu().numpy(), o_val, rtol=1e-4)
 
 
+@pytest.mark.parametrize("impl", ["tcgen05", "simt"])
 @pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
-def test_direct_map_and_argmax(ctx, combine):
+def test_direct_map_and_argmax(ctx, combine, impl):
     sc = S.small()
     T = 19
     fr, _ = O.synth(sc, 3, T)
     ref = O.direct_map(sc, fr, magnitude=combine == S.MAGNITUDE)
     fd = frames_to_dev(fr)
-    m = gh.location_decision_map(ctx, sc, fd, combine).cpu().numpy()
-    assert rel_map_err(m, ref) < MAP_TOL
-    idx, _ = gh.direct_argmax(ctx, sc, fd, combine)
-    assert_argmax_parity(ref, idx.cpu().numpy(), "direct")
+    ctx.set_direct_impl(impl)
+    try:
+        m = gh.location_decision_map(ctx, sc, fd, combine).cpu().numpy()
+        assert rel_map_err(m, ref) < MAP_TOL
+        idx, _ = gh.direct_argmax(ctx, sc, fd, combine)
+        assert_argmax_parity(ref, idx.cpu().numpy(), f"direct {impl}")
+    finally:
+        ctx.set_direct_impl("tcgen05")
+
+
+def test_direct_tcgen05_c2_scale(ctx):
+    # the c2 scene (40,000 bins x 3 pairs, N = 256), 130 trials: two trial
+    # tiles of 128 (ragged) through the tensor-core path
+    sc = S.baseline("c2")
+    T = 130
+    fr, _ = O.synth(sc, 0, T)
+    sub = np.arange(0, T, 13)
+    ref = O.direct_map(sc, fr[sub])
+    fd = frames_to_dev(fr)
+    m = gh.location_decision_map(ctx, sc, fd).cpu().numpy()
+    assert rel_map_err(m[sub], ref) < MAP_TOL
+    idx, _ = gh.direct_argmax(ctx, sc, fd)
+    assert_argmax_parity(ref, idx.cpu().numpy()[sub], "direct c2")
+    # per-element relative error on the peak neighbourhood (3xTF32 ~ fp32)
+    peak = ref.max(axis=1, keepdims=True)
+    big = ref > 0.1 * peak
+    assert (np.abs(m[sub] - ref)[big] / ref[big]).max() < 1e-4
 
 
 def test_edge_cases(ctx, small_scene):
