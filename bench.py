@@ -104,6 +104,29 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "NVML, 1 ms poll"}
 
 
+def tf32_peak_tflops(device: int) -> float:
+    """cuBLAS fp32 GEMM on the TF32 tensor cores, best of 5 (the TF32
+    counterpart of MEASURED_PEAKS.json's bf16 figure)."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=f"cuda:{device}")
+        b = torch.randn(n, n, device=f"cuda:{device}")
+        best = float("inf")
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -270,6 +293,41 @@ def run_ours(args, world, rank, local):
     ctx.synchronize()
     camp_ms = e0.elapsed_time(e1) / args.steps
 
+    # ---- direct method (BASELINE c2 "run both ways"): tcgen05 3xTF32
+    direct = None
+    if not args.no_direct:
+        for _ in range(2):
+            gh.direct_argmax(ctx, sc, frames)
+        ctx.synchronize()
+        ctx.reset_timing()
+        ctx.set_timing(True)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            d0.record(stream)
+            for _ in range(args.direct_steps):
+                didx, _ = gh.direct_argmax(ctx, sc, frames)
+            d1.record(stream)
+        ctx.synchronize()
+        ctx.set_timing(False)
+        dk_ms, dk_n = ctx.kernel_time("direct_umma")
+        dstep_ms = d0.elapsed_time(d1) / args.direct_steps
+        flops = 8.0 * N * G * P * T  # algorithmic: one complex MAC = 8 flops
+        tf32_peak = tf32_peak_tflops(local)
+        agree = float(np.mean(didx.cpu().numpy() == idx.cpu().numpy()))
+        direct = {"ms_per_step": dstep_ms, "kernel_ms": dk_ms / max(dk_n, 1),
+                  "trials_per_s": T * world / (dstep_ms * 1e-3),
+                  "value": units_step / (dstep_ms * 1e-3),
+                  "tflops_algorithmic": flops / (dk_ms / max(dk_n, 1) * 1e-3) / 1e12,
+                  "roofline": {"bound": "tensor", "unit": "TFLOP/s", "peak": tf32_peak,
+                               "peak_source": "torch.matmul fp32 8192^3 with TF32 tensor cores "
+                                              "(cuBLAS), measured in-run",
+                               "achieved": flops / (dk_ms / max(dk_n, 1) * 1e-3) / 1e12,
+                               "frac": flops / (dk_ms / max(dk_n, 1) * 1e-3) / 1e12 / tf32_peak,
+                               "executed_mma_factor": 3,
+                               "note": "3xTF32 issues 3 MMAs per algorithmic MAC"},
+                  "hop_direct_argmax_agreement": agree,
+                  "api": "gh_direct_argmax_d (tcgen05 kind::tf32, 3xTF32)"}
+
     if rank != 0:
         if dist:
             tdist.destroy_process_group()
@@ -309,6 +367,8 @@ def run_ours(args, world, rank, local):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if direct:
+        line["direct"] = direct
     if world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         oi, oc, _ = O.build_table(sc)
@@ -328,6 +388,8 @@ def main():
     ap.add_argument("--trials", type=int, default=0)
     ap.add_argument("--ref-trials", type=int, default=400)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-direct", action="store_true")
+    ap.add_argument("--direct-steps", type=int, default=3)
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
