@@ -211,6 +211,18 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->keys.release();
     c->misc.release();
     c->twiddle_buf.release();
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->ev_ready)
+      for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(c->ev_copied[b]);
+        cudaEventDestroy(c->ev_consumed[b]);
+      }
+    for (auto& p : c->pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -476,27 +488,57 @@ int gh_hop_estimate(gh_ctx* ctx, gh_table* table, const double* frames, int32_t 
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
     use_device(c);
-    const int64_t n = (int64_t)n_trials * t->P * t->N;
-    // frames (complex128 as the reference's FrameSet) -> device -> complex64
-    auto* d128 = static_cast<double2*>(c->frames.get(sizeof(double2) * n + sizeof(float2) * n +
-                                                     (sizeof(int64_t) + sizeof(float)) * n_trials));
-    auto* d64 = reinterpret_cast<float2*>(d128 + n);
-    auto* didx = reinterpret_cast<int64_t*>(d64 + n);
+    // Pipelined over trial chunks: the H2D copy of chunk i+1 (copy stream)
+    // overlaps the conversion + FFT + gather of chunk i (context stream).
+    // Frames arrive as complex128 (the reference's FrameSet element type).
+    const int64_t per = (int64_t)t->P * t->N;
+    int chunk = n_trials;
+    if (n_trials >= 1024) chunk = ((n_trials + 3) / 4 + 31) / 32 * 32;
+    const int n_chunks = (n_trials + chunk - 1) / chunk;
+    const size_t b128 = sizeof(double2) * per * chunk;
+    auto* base = static_cast<unsigned char*>(c->frames.get(
+        2 * b128 + sizeof(float2) * per * chunk + (sizeof(int64_t) + sizeof(float)) * n_trials));
+    double2* d128[2] = {reinterpret_cast<double2*>(base), reinterpret_cast<double2*>(base + b128)};
+    auto* d64 = reinterpret_cast<float2*>(base + 2 * b128);
+    auto* didx = reinterpret_cast<int64_t*>(d64 + per * chunk);
     auto* dval = reinterpret_cast<float*>(didx + n_trials);
-    GH_CUDA(cudaMemcpyAsync(d128, frames, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
-    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
-    {
-      gh::KTimer kt(c, "convert");
-      k_c128_to_c64<<<blocks, 256, 0, c->stream>>>(d128, d64, n);
-      GH_LAUNCHED(c);
+    if (!c->copy_stream) GH_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (!c->ev_ready) {
+      for (int b = 0; b < 2; ++b) {
+        GH_CUDA(cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+        GH_CUDA(cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
+      }
+      c->ev_ready = true;
     }
-    hop_argmax(c, t, d64, nullptr, n_trials, combine, didx, dval);
-    std::vector<float> hv(static_cast<size_t>(n_trials));
-    GH_CUDA(cudaMemcpyAsync(idx, didx, sizeof(int64_t) * n_trials, cudaMemcpyDeviceToHost, c->stream));
-    GH_CUDA(cudaMemcpyAsync(hv.data(), dval, sizeof(float) * n_trials, cudaMemcpyDeviceToHost,
-                            c->stream));
+    auto* hpin = static_cast<unsigned char*>(c->host_pinned((sizeof(int64_t) + sizeof(float)) * n_trials));
+    auto* hidx = reinterpret_cast<int64_t*>(hpin);
+    auto* hval = reinterpret_cast<float*>(hidx + n_trials);
+    for (int i = 0; i < n_chunks; ++i) {
+      const int b = i & 1;
+      const int t0 = i * chunk;
+      const int tc = std::min(chunk, n_trials - t0);
+      const int64_t n = per * tc;
+      if (i >= 2) GH_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[b], 0));
+      GH_CUDA(cudaMemcpyAsync(d128[b], frames + 2 * per * t0, sizeof(double2) * n,
+                              cudaMemcpyHostToDevice, c->copy_stream));
+      GH_CUDA(cudaEventRecord(c->ev_copied[b], c->copy_stream));
+      GH_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+      const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
+      {
+        gh::KTimer kt(c, "convert");
+        k_c128_to_c64<<<blocks, 256, 0, c->stream>>>(d128[b], d64, n);
+        GH_LAUNCHED(c);
+      }
+      GH_CUDA(cudaEventRecord(c->ev_consumed[b], c->stream));
+      hop_argmax(c, t, d64, nullptr, tc, combine, didx + t0, dval + t0);
+      GH_CUDA(cudaMemcpyAsync(hidx + t0, didx + t0, sizeof(int64_t) * tc, cudaMemcpyDeviceToHost,
+                              c->stream));
+      GH_CUDA(cudaMemcpyAsync(hval + t0, dval + t0, sizeof(float) * tc, cudaMemcpyDeviceToHost,
+                              c->stream));
+    }
     GH_CUDA(cudaStreamSynchronize(c->stream));
-    for (int32_t i = 0; i < n_trials; ++i) val[i] = hv[static_cast<size_t>(i)];
+    std::memcpy(idx, hidx, sizeof(int64_t) * n_trials);
+    for (int32_t i = 0; i < n_trials; ++i) val[i] = hval[i];
   });
 }
 

@@ -179,8 +179,10 @@ __global__ void __launch_bounds__(kThreads) k_direct_umma(UmmaArgs a) {
     __syncthreads();
     for (int k0 = 0; k0 < K2; k0 += BK) {
       // ---- A: 128 trials x 32 tf32 = 8 chunks of (2 complex samples)
+      // rows fastest across lanes: consecutive 16-byte rows of a core matrix
+      // column -> conflict-free STS.128 (k-chunk-fastest order is 8-way)
       for (int e = threadIdx.x; e < BT * KCH; e += kThreads) {
-        const int row = e / KCH, kc = e % KCH;
+        const int kc = e / BT, row = e % BT;
         const int t = t0 + row;
         const int n = (k0 >> 1) + 2 * kc;  // first complex sample of the chunk
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(kThreads) k_direct_umma(UmmaArgs a) {
       //      re column: (cos n, sin n, cos n+1, sin n+1)
       //      im column: (-sin n, cos n, -sin n+1, cos n+1)
       for (int e = threadIdx.x; e < BGU * KCH; e += kThreads) {
-        const int j = e / KCH, kc = e % KCH;
+        const int kc = e / BGU, j = e % BGU;
         const int n = (k0 >> 1) + 2 * kc;
         float c0 = 0.f, s0 = 0.f, c1 = 0.f, s1 = 0.f;
         const double rj = rho[j];

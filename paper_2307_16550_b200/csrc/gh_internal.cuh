@@ -64,6 +64,22 @@ struct Ctx {
   Buffer spectra, frames, keys, misc, twiddle_buf;
   int twiddle_m = 0;
   int direct_impl = 0;  // 0: tcgen05 3xTF32, 1: CUDA-core fp32 (reference path)
+  // host-buffer entry points: copy stream, double-buffer events, pinned staging
+  cudaStream_t copy_stream = nullptr;
+  bool ev_ready = false;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* host_pinned(size_t n) {
+    if (n > pinned_bytes) {
+      if (pinned) cudaFreeHost(pinned);
+      pinned = nullptr;
+      pinned_bytes = 0;
+      check_cuda(cudaMallocHost(&pinned, n), "cudaMallocHost");
+      pinned_bytes = n;
+    }
+    return pinned;
+  }
   // optional per-kernel CUDA-event timing on the context stream
   bool timing = false;
   struct Pending {
