@@ -169,8 +169,9 @@ class Context:
         _check(lib().gh_ctx_reset_timing(self.h))
 
     def set_direct_impl(self, impl: str) -> None:
-        """'tcgen05' (default, 3xTF32 tensor cores) or 'simt' (CUDA-core fp32)."""
-        _check(lib().gh_ctx_set_direct_impl(self.h, {"tcgen05": 0, "simt": 1}[impl]))
+        """'tcgen05' (default: warp-specialised 3xTF32 tensor-core pipeline),
+        'tcgen05_v1' (single-stage tensor-core kernel) or 'simt' (CUDA-core fp32)."""
+        _check(lib().gh_ctx_set_direct_impl(self.h, {"tcgen05": 0, "simt": 1, "tcgen05_v1": 2}[impl]))
 
     def smem_peak_gbps(self) -> float:
         v = C.c_double()

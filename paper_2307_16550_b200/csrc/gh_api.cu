@@ -267,7 +267,8 @@ int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     if (!c) fail(GH_EINVAL, "ctx: null argument");
-    if (impl != 0 && impl != 1) fail(GH_EINVAL, "ctx: direct impl must be 0 (tcgen05) or 1 (simt)");
+    if (impl < 0 || impl > 2)
+      fail(GH_EINVAL, "ctx: direct impl must be 0 (tcgen05), 1 (simt) or 2 (tcgen05 v1)");
     c->direct_impl = impl;
   });
 }

@@ -303,6 +303,252 @@ __global__ void __launch_bounds__(kThreads) k_direct_umma(UmmaArgs a) {
   }
 }
 
+// ============================================================ v2
+// Warp-specialised pipeline. 16 warps:
+//   warps 8-15  producers: per stage (pair p, 32-wide K chunk) write A
+//               (128 trials, frames split into tf32 big/small) and B
+//               (128 bins x re/im = 256 rows of steering, generated by an
+//               fp64-seeded phasor recurrence) into a 2-stage smem ring;
+//   warp 0 lane 0  MMA issuer: 3 x 4 tcgen05.mma (M=128, N=256, K=8) per
+//               stage into one 256-column TMEM accumulator;
+//   warps 0-7  epilogue: after each pair, warp w reads TMEM lane quarter
+//               w%4, bins [64(w/4), +64), and adds |z|^2 to registers.
+// mbarriers: full[s] (256 producer arrivals), empty[s] (MMA commit),
+// acc_full (MMA commit after a pair), acc_empty (8 epilogue warps).
+namespace v2 {
+
+constexpr int BG = 128;           // bins per CTA
+constexpr int NC = 2 * BG;        // MMA N
+constexpr int kThreads = 512;
+constexpr int kProd = 256;        // producer threads (warps 8..15)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BT * BK * 4;   // 16 KB
+constexpr int B_BYTES = NC * BK * 4;   // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int LBOA = BT / 8 * 128;
+constexpr int LBOB = NC / 8 * 128;
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NC >> 3) << 17) |
+                             ((uint32_t)(BT >> 4) << 24);
+
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc2), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
+                                            float4 v) {
+  uint4 b, s;
+  b.x = tf32_rna(v.x); s.x = __float_as_uint(v.x - __uint_as_float(b.x));
+  b.y = tf32_rna(v.y); s.y = __float_as_uint(v.y - __uint_as_float(b.y));
+  b.z = tf32_rna(v.z); s.z = __float_as_uint(v.z - __uint_as_float(b.z));
+  b.w = tf32_rna(v.w); s.w = __float_as_uint(v.w - __uint_as_float(b.w));
+  *reinterpret_cast<uint4*>(big + off) = b;
+  *reinterpret_cast<uint4*>(sml + off) = s;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full, acc_empty;
+  __shared__ uint32_t tmem_base_s;
+  __shared__ double rho_s[BG];    // r / N of the current pair (producers)
+  __shared__ float2 wst_s[BG];    // exp(j 2 pi rho): one-sample phasor step
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.y * BT;           // trial tile (slow) ...
+  const int64_t g0 = (int64_t)blockIdx.x * BG;  // ... bin tile (fast): A stays in L2
+  const int KC = (2 * a.N) / BK;            // K chunks per pair
+  const int n_stage = a.P * KC;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_s)),
+                 "r"(NC));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kProd);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp >= 8) {
+    // ======================= producers
+    const int pt = threadIdx.x - 256;  // 0..255
+    const int row = pt & 127, half = pt >> 7;
+    const double inv_n = 1.0 / (double)a.N;
+    for (int i = 0; i < n_stage; ++i) {
+      const int p = i / KC, kc0 = i - p * KC;
+      const int s = i % STAGES;
+      const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+      if (kc0 == 0) {
+        // new pair: ranges of this CTA's bins (producers only, named barrier 1)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (pt < BG) {
+          const int64_t g = g0 + pt;
+          double r = 0.0;
+          if (g < a.G) {
+            double x[3];
+            dgrid_point(a.grid, g, x);
+            const double* tp = a.txrx + 6 * p;
+            r = __dmul_rn(a.scale, __dadd_rn(dnorm3(tp, x[0], x[1], x[2]),
+                                             dnorm3(tp + 3, x[0], x[1], x[2])));
+          }
+          const double rho = r * inv_n;
+          rho_s[pt] = rho;
+          float sw, cw;
+          sincospif((float)(2.0 * (rho - floor(rho))), &sw, &cw);
+          wst_s[pt] = make_float2(cw, sw);
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+      mbar_wait(&empty[s], ph ^ 1u);
+      unsigned char* base = sm + s * STAGE_BYTES;
+      unsigned char* abig = base;
+      unsigned char* asml = base + A_BYTES;
+      unsigned char* bbig = base + 2 * A_BYTES;
+      unsigned char* bsml = bbig + B_BYTES;
+      const int nb = kc0 * (BK / 2);  // first complex sample of the chunk
+      // A: trial row, 4 of the 8 16-byte chunks (2 complex samples each)
+      {
+        const int t = t0 + row;
+        const float4* src = reinterpret_cast<const float4*>(a.frames + ((int64_t)t * a.P + p) * a.N + nb);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int kc = half * 4 + c;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (t < a.T && nb + 2 * kc < a.N) v = __ldg(src + kc);
+          split_store(abig, asml, kmaj_off(row, kc, LBOA), v);
+        }
+      }
+      // B: bin `row`, samples nb + 8*half .. +7 (4 chunks), re and im rows
+      {
+        const int n_first = nb + 8 * half;
+        const double ph0 = rho_s[row] * (double)n_first;
+        float sn, cn;
+        sincospif((float)(2.0 * (ph0 - floor(ph0))), &sn, &cn);
+        const float2 w = wst_s[row];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float c0 = cn, s0 = sn;
+          float c1 = c0 * w.x - s0 * w.y, s1 = c0 * w.y + s0 * w.x;
+          cn = c1 * w.x - s1 * w.y;
+          sn = c1 * w.y + s1 * w.x;
+          const int kc = half * 4 + c;
+          if (n_first + 2 * c + 1 >= a.N) {  // beyond the frame: zero steering
+            c1 = s1 = 0.f;
+          }
+          const bool in0 = n_first + 2 * c < a.N;
+          split_store(bbig, bsml, kmaj_off(row, kc, LBOB),
+                      in0 ? make_float4(c0, s0, c1, s1) : make_float4(0.f, 0.f, 0.f, 0.f));
+          split_store(bbig, bsml, kmaj_off(BG + row, kc, LBOB),
+                      in0 ? make_float4(-s0, c0, -s1, c1) : make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[s]);
+    }
+  } else {
+    // ======================= MMA issuer (warp 0 lane 0) + epilogue (warps 0-7)
+    const int q = warp & 3, h = warp >> 2;
+    float pw[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) pw[j] = 0.f;
+    for (int p = 0; p < a.P; ++p) {
+      if (warp == 0) {
+        if (lane == 0) {
+          if (p > 0) {
+            mbar_wait(&acc_empty, (uint32_t)(p - 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          for (int kc0 = 0; kc0 < KC; ++kc0) {
+            const int i = p * KC + kc0;
+            const int s = i % STAGES;
+            mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t base = smem_u32(sm + s * STAGE_BYTES);
+            const uint32_t ab = base, as_ = base + A_BYTES;
+            const uint32_t bb = base + 2 * A_BYTES, bs = bb + B_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              const uint64_t dab = umma_desc(ab + 2 * k * LBOA, LBOA, 128);
+              const uint64_t das = umma_desc(as_ + 2 * k * LBOA, LBOA, 128);
+              const uint64_t dbb = umma_desc(bb + 2 * k * LBOB, LBOB, 128);
+              const uint64_t dbs = umma_desc(bs + 2 * k * LBOB, LBOB, 128);
+              mma(tmem, dab, dbb, (kc0 > 0 || k > 0) ? 1u : 0u);
+              mma(tmem, dab, dbs, 1u);
+              mma(tmem, das, dbb, 1u);
+            }
+            mma_commit(&empty[s]);
+          }
+          mma_commit(&acc_full);
+        }
+        __syncwarp();
+      }
+      // epilogue of pair p
+      mbar_wait(&acc_full, (uint32_t)p & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t row_addr = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        float re[16], im[16];
+        tmem_ld16(row_addr + 64 * h + c, re);
+        tmem_ld16(row_addr + BG + 64 * h + c, im);
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          const float v = re[i2] * re[i2] + im[i2] * im[i2];
+          pw[c + i2] += a.mag ? sqrtf(v) : v;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty);
+    }
+    // final: map or per-trial argmax over this warp's 64 bins
+    const int t = t0 + q * 32 + lane;
+    const int64_t gb0 = g0 + 64 * h;
+    if (t < a.T) {
+      if (a.map) {
+        for (int j = 0; j < 64; ++j)
+          if (gb0 + j < a.G) a.map[(int64_t)t * a.G + gb0 + j] = pw[j];
+      } else {
+        float bv = -1.f;
+        int bj = -1;
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (gb0 + j < a.G && pw[j] > bv) {
+            bv = pw[j];
+            bj = j;
+          }
+        if (bj >= 0)
+          atomicMax(a.keys + t, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                    (0xffffffffull - (unsigned long long)(gb0 + bj)));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NC));
+  }
+}
+
+}  // namespace v2
+
 }  // namespace
 
 void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
@@ -322,6 +568,20 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
   a.keys = keys_d;
   if (a.P > kMaxPairs) fail(GH_EINVAL, "direct: at most 64 TX-RX pairs");
   if (a.N % 2) fail(GH_EINVAL, "direct: n_samples must be even");
+  if (ctx->direct_impl == 0) {
+    if ((2 * a.N) % BK) fail(GH_EINVAL, "direct: n_samples must be a multiple of 16");
+    const int64_t gbt = (a.G + v2::BG - 1) / v2::BG;
+    const int tt = (T + BT - 1) / BT;
+    if (tt > 65535) fail(GH_EINVAL, "direct: too many trials for one launch");
+    const size_t smem2 = v2::STAGES * v2::STAGE_BYTES;
+    GH_CUDA(cudaFuncSetAttribute(v2::k_direct_umma2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem2)));
+    dim3 grid2(static_cast<unsigned>(gbt), tt);
+    KTimer kt(ctx, "direct_umma");
+    v2::k_direct_umma2<<<grid2, v2::kThreads, smem2, ctx->stream>>>(a);
+    GH_LAUNCHED(ctx);
+    return;
+  }
   const int64_t gb = (a.G + BGU - 1) / BGU;
   if (gb > 65535) fail(GH_EINVAL, "direct: grid too large for one launch");
   const size_t smem = 2 * TILE_BYTES_A + 2 * TILE_BYTES_B;

@@ -156,7 +156,7 @@ def test_campaign_matches_oracle_campaign(ctx):
     assert np.allclose(g_val.cpu().numpy(), o_val, rtol=1e-4)
 
 
-@pytest.mark.parametrize("impl", ["tcgen05", "simt"])
+@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_v1", "simt"])
 @pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
 def test_direct_map_and_argmax(ctx, combine, impl):
     sc = S.small()
