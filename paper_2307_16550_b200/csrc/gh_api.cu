@@ -211,6 +211,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->keys.release();
     c->misc.release();
     c->twiddle_buf.release();
+    c->aprep.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)

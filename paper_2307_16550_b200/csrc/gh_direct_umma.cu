@@ -54,6 +54,7 @@ struct UmmaArgs {
   int mag;
   float* map;
   unsigned long long* keys;
+  const unsigned char* aprep;  // v2: prepared A stage blocks (k_prep_a)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -341,6 +342,50 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// raise the barrier's expected transaction bytes (no arrival)
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// TMA bulk copy global -> shared, completing `bytes` on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
+                                            float4 v);
+
+// A operand prepared once per call: frames split into tf32 big/small and
+// laid out exactly as one stage's smem tile (canonical K-major), so a stage
+// is one contiguous 32 KB block: [trial tile][pair][k chunk][big | small].
+__global__ void k_prep_a(const float2* __restrict__ frames, int T, int P, int N,
+                         unsigned char* __restrict__ out) {
+  const int KC = (2 * N) / BK;
+  const int64_t n16 = (int64_t)((T + BT - 1) / BT) * BT * P * (N / 2);  // 16-byte chunks
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n16;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    // e -> (trial tile, pair, k chunk, 16-byte chunk in stage, row), row fastest
+    const int row = (int)(e % BT);
+    int64_t r = e / BT;
+    const int c16 = (int)(r % (N / 2));  // global 16-byte chunk along K (2 samples)
+    r /= (N / 2);
+    const int p = (int)(r % P);
+    const int tt = (int)(r / P);
+    const int t = tt * BT + row;
+    const int kc = c16 / KCH, kin = c16 % KCH;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < T) v = __ldg(reinterpret_cast<const float4*>(frames + ((int64_t)t * P + p) * N) + c16);
+    unsigned char* blk = out + (((int64_t)tt * P + p) * KC + kc) * (2 * A_BYTES);
+    split_store(blk, blk + A_BYTES, kmaj_off(row, kin, LBOA), v);
+  }
+}
+
 __device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
                                             float4 v) {
   uint4 b, s;
@@ -422,18 +467,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
       unsigned char* bbig = base + 2 * A_BYTES;
       unsigned char* bsml = bbig + B_BYTES;
       const int nb = kc0 * (BK / 2);  // first complex sample of the chunk
-      // A: trial row, 4 of the 8 16-byte chunks (2 complex samples each)
-      {
-        const int t = t0 + row;
-        const float4* src = reinterpret_cast<const float4*>(a.frames + ((int64_t)t * a.P + p) * a.N + nb);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int kc = half * 4 + c;
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (t < a.T && nb + 2 * kc < a.N) v = __ldg(src + kc);
-          split_store(abig, asml, kmaj_off(row, kc, LBOA), v);
-        }
+      // A: the prepared big|small stage block, one TMA bulk copy; its bytes
+      // complete on full[s] together with the producers' arrivals
+      if (pt == 0) {
+        const unsigned char* src =
+            a.aprep + (((int64_t)blockIdx.y * a.P + p) * KC + kc0) * (2 * A_BYTES);
+        mbar_expect_tx(&full[s], 2 * A_BYTES);
+        bulk_g2s(abig, src, 2 * A_BYTES, &full[s]);
       }
+      (void)asml;
       // B: bin `row`, samples nb + 8*half .. +7 (4 chunks), re and im rows
       {
         const int n_first = nb + 8 * half;
@@ -574,6 +616,17 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
     const int tt = (T + BT - 1) / BT;
     if (tt > 65535) fail(GH_EINVAL, "direct: too many trials for one launch");
     const size_t smem2 = v2::STAGES * v2::STAGE_BYTES;
+    const int KC = (2 * a.N) / BK;
+    const size_t aprep_bytes = (size_t)tt * a.P * KC * (2 * TILE_BYTES_A);
+    a.aprep = static_cast<const unsigned char*>(ctx->aprep.get(aprep_bytes));
+    {
+      KTimer kt(ctx, "direct_prep");
+      const int64_t n16 = (int64_t)tt * BT * a.P * (a.N / 2);
+      const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 148LL * 32));
+      v2::k_prep_a<<<blocks, 256, 0, ctx->stream>>>(frames_d, T, a.P, a.N,
+                                                    const_cast<unsigned char*>(a.aprep));
+      GH_LAUNCHED(ctx);
+    }
     GH_CUDA(cudaFuncSetAttribute(v2::k_direct_umma2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem2)));
     dim3 grid2(static_cast<unsigned>(gbt), tt);
