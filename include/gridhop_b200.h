@@ -162,6 +162,19 @@ int gh_hop_estimate(gh_ctx* ctx, gh_table* t, const double* frames,
 int gh_campaign_hop_d(gh_ctx* ctx, gh_table* t, const gh_campaign* camp,
                       uint64_t trial0, int32_t n_trials, int32_t combine,
                       int64_t* idx_d, float* val_d);
+/* Multi-target peak pick (BASELINE c3): per trial the k <= 8 best local
+ * maxima of the hop map (a bin beats every smaller-index neighbour strictly
+ * and every larger-index neighbour or ties; 8-neighbourhood in 2-D, 26 in
+ * 3-D), ranked by (value desc, bin asc). idx_d int64 [T][k] (-1 = none),
+ * val_d fp32 [T][k]. Campaign form synthesises the trials on the device. */
+int gh_hop_topk_d(gh_ctx* ctx, gh_table* t, const float* frames_d, int32_t n_trials,
+                  int32_t combine, int32_t k, int64_t* idx_d, float* val_d);
+int gh_campaign_hop_topk_d(gh_ctx* ctx, gh_table* t, const gh_campaign* camp, uint64_t trial0,
+                           int32_t n_trials, int32_t combine, int32_t k, int64_t* idx_d,
+                           float* val_d);
+/* The same peak pick on caller-provided maps fp32 [T][G] (e.g. direct maps). */
+int gh_topk_local_max_d(gh_ctx* ctx, const gh_grid* grid, const float* map_d, int32_t n_trials,
+                        int32_t k, int64_t* idx_d, float* val_d);
 /* location_decision_map (src/direct.cpp:90-144) for T trials at once as the
  * complex contraction Z_p = Y_p (T x N) . A_p^H (N x G) on the tensor cores
  * (tcgen05, 3xTF32), |.|^2 summed over pairs in the epilogue. */

@@ -86,6 +86,9 @@ def lib() -> C.CDLL:
             "gh_hop_argmax_d": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
             "gh_hop_estimate": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
             "gh_campaign_hop_d": (C.c_int, [vp, vp, P(CCampaign), u64, i32, i32, vp, vp]),
+            "gh_hop_topk_d": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
+            "gh_campaign_hop_topk_d": (C.c_int, [vp, vp, P(CCampaign), u64, i32, i32, i32, vp, vp]),
+            "gh_topk_local_max_d": (C.c_int, [vp, P(CGrid), vp, i32, i32, vp, vp]),
             "gh_direct_map_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp]),
             "gh_direct_argmax_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp, vp]),
         }
@@ -329,6 +332,41 @@ def campaign_hop(ctx: Context, table: HopTable, scene: Scene, trial0: int, n_tri
     camp = scene.c_campaign(snr_db)
     _check(lib().gh_campaign_hop_d(ctx.h, table.h, C.byref(camp), trial0, n_trials, combine,
                                    _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def hop_topk(ctx: Context, table: HopTable, frames, k: int, combine: int = POWER):
+    """Top-k local maxima of each trial's hop map (BASELINE c3): (idx [T,k], val [T,k])."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    T = frames.shape[0]
+    idx = torch.empty((T, k), dtype=torch.int64, device=frames.device)
+    val = torch.empty((T, k), dtype=torch.float32, device=frames.device)
+    _check(lib().gh_hop_topk_d(ctx.h, table.h, _ptr(frames), T, combine, k, _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def campaign_hop_topk(ctx: Context, table: HopTable, scene: Scene, trial0: int, n_trials: int,
+                      k: int, combine: int = POWER, snr_db=None):
+    torch = _torch()
+    dev = f"cuda:{ctx.device}"
+    idx = torch.empty((n_trials, k), dtype=torch.int64, device=dev)
+    val = torch.empty((n_trials, k), dtype=torch.float32, device=dev)
+    camp = scene.c_campaign(snr_db)
+    _check(lib().gh_campaign_hop_topk_d(ctx.h, table.h, C.byref(camp), trial0, n_trials, combine, k,
+                                        _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def topk_local_max(ctx: Context, scene: Scene, maps, k: int):
+    """Top-k local maxima of caller maps fp32 [T, G] on the device."""
+    torch = _torch()
+    T = maps.shape[0]
+    idx = torch.empty((T, k), dtype=torch.int64, device=maps.device)
+    val = torch.empty((T, k), dtype=torch.float32, device=maps.device)
+    g = scene.c_grid()
+    _check(lib().gh_topk_local_max_d(ctx.h, C.byref(g), _ptr(maps.contiguous()), T, k, _ptr(idx),
+                                     _ptr(val)))
     return idx, val
 
 

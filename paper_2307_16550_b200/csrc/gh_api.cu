@@ -166,6 +166,32 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
   if (h & 1) fail(GH_ERUNTIME, "scene outside unambiguous window");
 }
 
+// Top-K local maxima per trial (BASELINE c3): maps of a trial chunk are
+// materialised (<= 1 GiB), then k_topk_localmax picks the peaks.
+void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
+              int combine, int K, int64_t* idx_d, float* val_d) {
+  gh::build_plan(c, t);
+  const int tb = t->plan.tb;
+  int64_t chunk = (int64_t(1) << 28) / std::max<int64_t>(t->G, 1);
+  chunk = std::max<int64_t>(tb, chunk / tb * tb);
+  chunk = std::min<int64_t>(chunk, (T + tb - 1) / tb * tb);
+  float* map = static_cast<float*>(c->mapbuf.get(sizeof(float) * chunk * t->G));
+  for (int t0 = 0; t0 < T; t0 += static_cast<int>(chunk)) {
+    const int tc = static_cast<int>(std::min<int64_t>(chunk, T - t0));
+    gh::SynthParams sc{};
+    const gh::SynthParams* spc = nullptr;
+    if (sp) {
+      sc = *sp;
+      sc.trial0 += static_cast<uint64_t>(t0);
+      spc = &sc;
+    }
+    const float2* fr = frames ? frames + (int64_t)t0 * t->P * t->N : nullptr;
+    void* spec = gather_spectra(c, t, fr, spc, tc, combine);
+    gh::launch_gather(c, t, spec, tc, combine, map, nullptr);
+    gh::launch_topk(c, map, tc, t->grid, K, idx_d + (int64_t)t0 * K, val_d + (int64_t)t0 * K);
+  }
+}
+
 __global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -212,6 +238,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->misc.release();
     c->twiddle_buf.release();
     c->aprep.release();
+    c->mapbuf.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)
@@ -558,6 +585,56 @@ int gh_campaign_hop_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp, uin
     // wrap mode always: the table was built against the same scene
     const gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, 1);
     hop_argmax(c, t, nullptr, &sp, n_trials, combine, idx_d, val_d);
+  });
+}
+
+int gh_hop_topk_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                  int32_t combine, int32_t k, int64_t* idx_d, float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!frames_d || !idx_d || !val_d)))
+      fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (k < 1 || k > 8) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    hop_topk(c, t, reinterpret_cast<const float2*>(frames_d), nullptr, n_trials, combine, k, idx_d,
+             val_d);
+  });
+}
+
+int gh_campaign_hop_topk_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp, uint64_t trial0,
+                           int32_t n_trials, int32_t combine, int32_t k, int64_t* idx_d,
+                           float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!idx_d || !val_d)))
+      fail(GH_EINVAL, "campaign: null argument");
+    check_combine(combine);
+    if (k < 1 || k > 8) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    const gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, 1);
+    hop_topk(c, t, nullptr, &sp, n_trials, combine, k, idx_d, val_d);
+  });
+}
+
+int gh_topk_local_max_d(gh_ctx* ctx, const gh_grid* grid, const float* map_d, int32_t n_trials,
+                        int32_t k, int64_t* idx_d, float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!map_d || !idx_d || !val_d)))
+      fail(GH_EINVAL, "top-k: null argument");
+    grid_size(grid);
+    if (k < 1 || k > 8) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::launch_topk(c, map_d, n_trials, *grid, k, idx_d, val_d);
   });
 }
 

@@ -61,7 +61,7 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf;
   int twiddle_m = 0;
   int direct_impl = 0;  // 0: tcgen05 3xTF32, 1: CUDA-core fp32 (reference path)
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
@@ -224,6 +224,8 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
                    float* map_d, unsigned long long* keys_d);
 void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
                         int64_t* idx_d, float* val_d);
+void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t* idx_d,
+                 float* val_d);
 void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const float2* frames_d, int T, int combine, float* map_d,
                      unsigned long long* keys_d);

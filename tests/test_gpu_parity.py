@@ -209,3 +209,93 @@ def test_edge_cases(ctx, small_scene):
     ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
     idx, _ = gh.hop_argmax(ctx, t, frames_to_dev(fr))
     assert_argmax_parity(ref, idx.cpu().numpy(), "T=1")
+
+
+def topk_parity(ref_maps, gidx, sc, k, what):
+    bad = []
+    for t, m in enumerate(ref_maps):
+        oi, ov = O.topk_local_max(sc, m, k)
+        gi = gidx[t]
+        for j in range(k):
+            if oi[j] == gi[j]:
+                continue
+            # allowed only when the two candidates are a near-tie in value
+            a = m[oi[j]] if oi[j] >= 0 else 0.0
+            b = m[gi[j]] if gi[j] >= 0 else 0.0
+            if abs(a - b) > TIE_TOL * m.max():
+                bad.append((t, j, oi[j], gi[j], a, b))
+    assert not bad, f"{what}: top-k mismatches {bad[:4]}"
+
+
+def test_hop_topk_multi_target(ctx):
+    sc = S.small(n_targets=3, amp_mode=S.AMP_CGAUSS_PER_PAIR, snr_mode=S.SNR_UNIFORM_PER_PAIR,
+                 snr_lo=5.0, snr_hi=20.0, nx=30, ny=26, scheme=S.NEAREST)
+    T, K = 21, 3
+    fr, _ = O.synth(sc, 0, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    t = gh.precompute_hop_table(ctx, sc)
+    gidx, gval = gh.hop_topk(ctx, t, frames_to_dev(fr), K)
+    topk_parity(ref, gidx.cpu().numpy(), sc, K, "small top-3")
+    # campaign form (synthesis on the device) picks the same peaks
+    cidx, _ = gh.campaign_hop_topk(ctx, t, sc, 0, T, K)
+    topk_parity(ref, cidx.cpu().numpy(), sc, K, "campaign top-3")
+    # the same kernel on caller maps
+    m = gh.hop_decision_map(ctx, t, frames_to_dev(fr))
+    midx, _ = gh.topk_local_max(ctx, sc, m, K)
+    topk_parity(ref, midx.cpu().numpy(), sc, K, "maps top-3")
+
+
+def test_c3_full_grid_top5(ctx):
+    # BASELINE c3 at full size: 10^6 bins, 16 pairs, N = 1024, M = 4096,
+    # tiled 32-trial plan; a few trials against the oracle
+    sc = S.baseline("c3")
+    T, K = 6, 5
+    t = gh.precompute_hop_table(ctx, sc)
+    gi_, _ = t.download()
+    oi, oc, _ = O.build_table(sc)
+    assert np.array_equal(gi_, oi)
+    fr, truth = O.synth(sc, 0, T)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    gidx, _ = gh.hop_topk(ctx, t, frames_to_dev(fr), K)
+    topk_parity(ref, gidx.cpu().numpy(), sc, K, "c3 top-5")
+    cidx, _ = gh.campaign_hop_topk(ctx, t, sc, 0, T, K)
+    topk_parity(ref, cidx.cpu().numpy(), sc, K, "c3 campaign top-5")
+
+
+@pytest.mark.parametrize("scheme", [S.POLY3, S.POLAR])
+def test_c4_geometry_tiled_complex(ctx, scheme):
+    # c4 stations/waveform (16 pairs, N = 512, os = 2, K = 3) on a 160 x 160
+    # sub-grid: the tiled complex-spectrum plan at realistic tile sizes
+    c4 = S.baseline("c4")
+    sc = c4.with_(grid_n=(160, 160, 1), grid_origin=(-15.9, -15.9, 0.0), scheme=scheme,
+                  area_lo=(-16.0, -16.0, 0.0), area_hi=(16.0, 16.0, 0.0))
+    T = 33
+    oi, oc, _ = O.build_table(sc)
+    t = gh.precompute_hop_table(ctx, sc)
+    gi_, gc_ = t.download()
+    assert np.array_equal(gi_, oi) and np.abs(gc_ - oc).max() < 1e-9
+    fr, _ = O.synth(sc, 0, T, snr_db=0.0)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, t, fd).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, _ = gh.campaign_hop(ctx, t, sc, 0, T, snr_db=0.0)
+    assert_argmax_parity(ref, idx.cpu().numpy(), f"c4 scheme {scheme}")
+
+
+def test_campaign_statistics_match_oracle(ctx):
+    # RMSE / hit-ratio curve points (c1 scene, 3 SNRs): identical estimates
+    # give identical statistics
+    from paper_2307_16550_b200 import distributed as D
+    sc = S.baseline("c1")
+    T = 96
+    oi, oc, _ = O.build_table(sc)
+    t = gh.precompute_hop_table(ctx, sc)
+    for snr in (0.0, 10.0, 20.0):
+        o_idx, _ = O.campaign_hop(sc, oi, oc, 0, T, snr_db=snr)
+        g_idx, _ = gh.campaign_hop(ctx, t, sc, 0, T, snr_db=snr)
+        _, truth = O.synth(sc, 0, T, snr_db=snr)
+        so = D.campaign_stats(sc, o_idx, truth)
+        sg = D.campaign_stats(sc, g_idx.cpu().numpy(), truth)
+        assert np.allclose(so, sg), (snr, so, sg)
