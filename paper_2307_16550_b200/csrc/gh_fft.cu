@@ -406,8 +406,12 @@ constexpr int kFxThreads = 256;
 template <int LN, int LOS, int LROWS>
 struct Fx {
   static constexpr int N = 1 << LN, OS = 1 << LOS, M = N * OS, ROWS = 1 << LROWS;
-  // padded sub-FFT stride, odd so the os sub-rows of one bin hit distinct banks
-  static constexpr int SUBP = N + N / 16 + 1;
+  // padded sub-FFT stride, SUBP = 16/os (mod 16) float2: the os sub-rows
+  // holding consecutive output bins k = os*m + j land 32/os banks apart, so
+  // the epilogue's reads (consecutive k across lanes) are conflict-free
+  static constexpr int SUBP_BASE = N + N / 16;
+  static constexpr int SUBP_WANT = OS > 1 ? 16 / OS : 0;
+  static constexpr int SUBP = SUBP_BASE + ((SUBP_WANT - SUBP_BASE % 16) + 16) % 16;
   static constexpr int PITCH = OS * SUBP + ((OS * SUBP) % 2 == 0 ? 1 : 0);
   static constexpr int NP = (LN + 3) / 4;
   static constexpr int lr(int ps) { return LN - 4 * ps >= 4 ? 4 : LN - 4 * ps; }
@@ -497,6 +501,23 @@ __global__ void __launch_bounds__(kFxThreads) k_fft_fixed(FftArgs a) {
       }
     }
   }
+  // frames of the next row group are fetched into registers while the
+  // current group runs its passes (hides the HBM latency behind barriers)
+  constexpr int LPT = (R * N + kFxThreads - 1) / kFxThreads;
+  float2 pre[LPT];
+  auto fetch = [&](int g) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) {
+      const int e = threadIdx.x + u * kFxThreads;
+      float2 v = make_float2(0.f, 0.f);
+      if (e < R * N) {
+        const int t = tb * a.tb + g + (e >> LN);
+        if (t < a.T) v = __ldg(a.frames + ((int64_t)t * a.P + p) * N + (e & (N - 1)));
+      }
+      pre[u] = v;
+    }
+  };
+  if (!a.synth) fetch(0);
   for (int g0 = 0; g0 < a.tb; g0 += R) {
     if (a.synth && threadIdx.x < R) {
       const int t = tb * a.tb + g0 + threadIdx.x;
@@ -510,23 +531,23 @@ __global__ void __launch_bounds__(kFxThreads) k_fft_fixed(FftArgs a) {
       }
     }
     __syncthreads();
-#pragma unroll 4
-    for (int e = threadIdx.x; e < R * N; e += kFxThreads) {
+#pragma unroll
+    for (int u = 0; u < LPT; ++u) {
+      const int e = threadIdx.x + u * kFxThreads;
+      if (e >= R * N) break;
       const int r = e >> LN;
       const int n = e & (N - 1);
-      const int t = tb * a.tb + g0 + r;
-      float2 v = make_float2(0.f, 0.f);
-      if (t < a.T) {
-        if (a.synth)
-          v = synth_sample(rsm[r], a.sp.camp.n_targets, n, inv_n);
-        else
-          v = a.frames[((int64_t)t * a.P + p) * N + n];
+      float2 v = pre[u];
+      if (a.synth) {
+        const int t = tb * a.tb + g0 + r;
+        v = t < a.T ? synth_sample(rsm[r], a.sp.camp.n_targets, n, inv_n) : make_float2(0.f, 0.f);
       }
       float2* row = buf0 + r * F::PITCH + pad_c(n);
       row[0] = v;
 #pragma unroll
       for (int j = 1; j < F::OS; ++j) row[j * F::SUBP] = cmul(v, __ldg(a.tw + j * n));
     }
+    if (!a.synth && g0 + R < a.tb) fetch(g0 + R);
     __syncthreads();
     const float2* sm = fixed_passes<LN, LOS, LROWS, 0>(buf0, buf1, ptw);
     if (a.out_kind == FFT_NATURAL) {
