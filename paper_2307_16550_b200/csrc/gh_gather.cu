@@ -30,7 +30,10 @@
 namespace gh {
 namespace {
 
-constexpr int kGatherThreads = 512;
+// threads per CTA: 24 warps for power (K = 1) plans, 16 for the complex
+// K = 3 plans (more registers per thread)
+template <bool K3>
+constexpr int gather_threads() { return K3 ? 512 : 768; }
 
 struct GatherArgs {
   const void* spec;       // [batches][P][M][TB] float or float2
@@ -98,7 +101,8 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
 template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
-__global__ void __launch_bounds__(kGatherThreads, 1) k_gather(GatherArgs a) {
+__global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a) {
+  constexpr int kGatherThreads = gather_threads<K3>();
   constexpr int ES = K3 ? 8 : 4;         // staged element bytes
   constexpr int L = TB * ES / 16;        // lanes per row (16 B each)
   constexpr int TPL = 16 / ES;           // trials per lane
@@ -296,7 +300,7 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   KTimer kt(ctx, "gather");
-  kern<<<grid, kGatherThreads, smem, ctx->stream>>>(a);
+  kern<<<grid, gather_threads<K3>(), smem, ctx->stream>>>(a);
   GH_LAUNCHED(ctx);
 }
 
