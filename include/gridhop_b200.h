@@ -118,6 +118,15 @@ int gh_measure_smem_peak(gh_ctx* ctx, double* gbps);
  * periodicity (interp.cpp:39-44) for aliasing scenes (BASELINE c1/c2). */
 int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                    int32_t scheme, int32_t wrap, gh_table** out);
+/* Location-grid shard (BASELINE c5): the operator for layers
+ * [layer_lo, layer_hi) of the grid's z axis (3-D grids) or y axis (2-D) —
+ * one contiguous range of global bins. Grid points are computed from the
+ * full grid, so rows are bit-identical to the full table's; every bin index
+ * this table reports (argmax, top-k) is global, so per-GPU shard winners
+ * merge with one all-reduce(max) of the 64-bit key. Maps are shard-local. */
+int gh_table_build_shard(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                         int32_t scheme, int32_t wrap, int32_t layer_lo,
+                         int32_t layer_hi, gh_table** out);
 /* load_hop_table (src/interp.cpp:318-389) analogue: host arrays in the
  * reference layout [bin][pair][K] (HopTable::entry_offset, interp.hpp:55-59);
  * coef = complex128 (re, im) pairs, NULL means all ones (K = 1). */

@@ -8,7 +8,8 @@ contraction — hand-written CUDA behind the C ABI in include/gridhop_b200.h.
 from . import scene
 from .scene import Scene, baseline, small
 from .api import (Context, HopTable, InvalidArgument, GridhopRuntimeError, DomainError, CudaError,
-                  precompute_hop_table, upload_hop_table, synthesize, fast_time_spectra,
+                  precompute_hop_table, precompute_hop_table_shard, upload_hop_table,
+                  synthesize, fast_time_spectra,
                   hop_decision_map, hop_argmax, hop_estimate, campaign_hop, hop_topk,
                   campaign_hop_topk, topk_local_max,
                   location_decision_map, direct_argmax, argmax_index, lib, exported_symbols)

@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
             "gh_ctx_set_direct_impl": (C.c_int, [vp, i32]),
             "gh_table_build": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, P(vp)]),
             "gh_table_upload": (C.c_int, [vp, P(CWave), P(CGrid), i32, vp, vp, P(vp)]),
+            "gh_table_build_shard": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, i32, i32, P(vp)]),
             "gh_table_info": (C.c_int, [vp, P(i64), P(i32), P(i32), P(i32), P(f64)]),
             "gh_table_download": (C.c_int, [vp, vp, vp]),
             "gh_table_destroy": (C.c_int, [vp]),
@@ -229,6 +230,21 @@ def precompute_hop_table(ctx: Context, scene: Scene, scheme: int | None = None,
                                 scene.scheme if scheme is None else scheme,
                                 int(scene.wrap if wrap is None else wrap), C.byref(h)))
     return HopTable(ctx, scene, h)
+
+
+def precompute_hop_table_shard(ctx: Context, scene: Scene, layer_lo: int, layer_hi: int,
+                               scheme: int | None = None, wrap: bool | None = None) -> HopTable:
+    """Location-grid shard (BASELINE c5): the operator for layers [lo, hi) of
+    z (3-D) / y (2-D); reported bin indices are global."""
+    h = C.c_void_p()
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_table_build_shard(ctx.h, C.byref(w), C.byref(g),
+                                      scene.scheme if scheme is None else scheme,
+                                      int(scene.wrap if wrap is None else wrap), layer_lo, layer_hi,
+                                      C.byref(h)))
+    t = HopTable(ctx, scene, h)
+    t.bin0, _ = scene.slab_bins(layer_lo, layer_hi)
+    return t
 
 
 def upload_hop_table(ctx: Context, scene: Scene, scheme: int, idx: np.ndarray,

@@ -87,6 +87,9 @@ gh::Table* new_table(gh::Ctx* c, const gh_wave* w, const gh_grid* g, int scheme)
   t->M = w->n_samples * w->os_range;
   t->scale = w->range_scale;
   t->grid = *g;
+  t->bin0 = 0;
+  t->slab_lo = 0;
+  t->slab_hi = g->n[2] > 1 ? g->n[2] : g->n[1];
   t->tx.assign(w->tx, w->tx + 3 * w->n_pairs);
   t->rx.assign(w->rx, w->rx + 3 * w->n_pairs);
   std::vector<double> h(static_cast<size_t>(t->P) * 6);
@@ -188,7 +191,11 @@ void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthPar
     const float2* fr = frames ? frames + (int64_t)t0 * t->P * t->N : nullptr;
     void* spec = gather_spectra(c, t, fr, spc, tc, combine);
     gh::launch_gather(c, t, spec, tc, combine, map, nullptr);
-    gh::launch_topk(c, map, tc, t->grid, K, idx_d + (int64_t)t0 * K, val_d + (int64_t)t0 * K);
+    // the table's (shard) lattice: its layers only; peaks reported globally
+    gh_grid lg = t->grid;
+    if (lg.n[2] > 1) lg.n[2] = t->slab_hi - t->slab_lo;
+    else lg.n[1] = t->slab_hi - t->slab_lo;
+    gh::launch_topk(c, map, tc, lg, K, t->bin0, idx_d + (int64_t)t0 * K, val_d + (int64_t)t0 * K);
   }
 }
 
@@ -375,6 +382,34 @@ int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_
   });
 }
 
+int gh_table_build_shard(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_t scheme,
+                         int32_t wrap, int32_t layer_lo, int32_t layer_hi, gh_table** out) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !out) fail(GH_EINVAL, "hop table: null argument");
+    use_device(c);
+    gh::Table* t = new_table(c, wave, grid, scheme);
+    const int axis_len = t->slab_hi;
+    if (layer_lo < 0 || layer_hi > axis_len || layer_lo >= layer_hi) {
+      free_table(t);
+      fail(GH_EINVAL, "hop table: shard layers outside the grid");
+    }
+    const int64_t layer = (int64_t)grid->n[0] * (grid->n[2] > 1 ? grid->n[1] : 1);
+    t->slab_lo = layer_lo;
+    t->slab_hi = layer_hi;
+    t->bin0 = layer_lo * layer;
+    t->G = (int64_t)(layer_hi - layer_lo) * layer;
+    try {
+      gh::build_table_device(c, t, wrap);
+      gh::build_plan(c, t);
+    } catch (...) {
+      free_table(t);
+      throw;
+    }
+    *out = reinterpret_cast<gh_table*>(t);
+  });
+}
+
 int gh_table_upload(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_t scheme,
                     const uint32_t* idx, const double* coef, gh_table** out) {
   return guarded([&] {
@@ -424,7 +459,14 @@ int gh_table_download(gh_table* table, uint32_t* idx, double* coef) {
     use_device(t->ctx);
     const int64_t n = t->G * t->P * t->K;
     if (idx) GH_CUDA(cudaMemcpy(idx, t->idx_d, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
-    if (coef) GH_CUDA(cudaMemcpy(coef, t->coef_d, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    if (coef && t->coef_d) {
+      GH_CUDA(cudaMemcpy(coef, t->coef_d, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    } else if (coef) {
+      for (int64_t i = 0; i < n; ++i) {  // nearest: unit coefficients (interp.cpp:92)
+        coef[2 * i] = 1.0;
+        coef[2 * i + 1] = 0.0;
+      }
+    }
   });
 }
 
@@ -634,7 +676,7 @@ int gh_topk_local_max_d(gh_ctx* ctx, const gh_grid* grid, const float* map_d, in
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
     use_device(c);
-    gh::launch_topk(c, map_d, n_trials, *grid, k, idx_d, val_d);
+    gh::launch_topk(c, map_d, n_trials, *grid, k, 0, idx_d, val_d);
   });
 }
 

@@ -42,7 +42,8 @@ struct GatherArgs {
   const uint16_t* rows;   // [entries][p4], 16-byte units
   const float2* coef3;    // [entries][P][3]
   gh_grid grid;
-  int64_t G;
+  int64_t G;              // bins of the table (shard)
+  int64_t bin0;           // global index of the shard's first bin
   int64_t chunk_bins;     // full plan
   int full;
   int P, p4, M, T;
@@ -52,7 +53,7 @@ struct GatherArgs {
 
 __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDesc& td,
                                               int64_t entry0, int64_t lb) {
-  if (a.full) return entry0 + lb;
+  if (a.full) return a.bin0 + entry0 + lb;
   const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
 }
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
 #pragma unroll
           for (int i = 0; i < TPL; ++i) {
             const int trial = tb * TB + v * TPL + i;
-            if (trial < a.T) a.map[(int64_t)trial * a.G + gb] = vals[i];
+            if (trial < a.T) a.map[(int64_t)trial * a.G + (gb - a.bin0)] = vals[i];
           }
         } else {
 #pragma unroll
@@ -342,6 +343,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.coef3 = pl.coef3_d;
   a.grid = t->grid;
   a.G = t->G;
+  a.bin0 = t->bin0;
   a.full = pl.full;
   a.P = t->P;
   a.p4 = pl.p4;
@@ -367,10 +369,13 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   if (!pl.k3) {
     // K = 1: the FFT epilogue already wrote power or magnitude
     if (pl.tb == 16) dispatch<16, false>(ctx, a, grid, smem, false, mapmode);
-    else dispatch<32, false>(ctx, a, grid, smem, false, mapmode);
+    else if (pl.tb == 32) dispatch<32, false>(ctx, a, grid, smem, false, mapmode);
+    else if (pl.tb == 8) dispatch<8, false>(ctx, a, grid, smem, false, mapmode);
+    else fail(GH_EINVAL, "gather: unsupported trial batch");
   } else {
-    if (pl.tb != 16) fail(GH_EINVAL, "gather: complex plans use 16-trial batches");
-    dispatch<16, true>(ctx, a, grid, smem, mag, mapmode);
+    if (pl.tb == 16) dispatch<16, true>(ctx, a, grid, smem, mag, mapmode);
+    else if (pl.tb == 8) dispatch<8, true>(ctx, a, grid, smem, mag, mapmode);
+    else fail(GH_EINVAL, "gather: unsupported trial batch");
   }
 }
 

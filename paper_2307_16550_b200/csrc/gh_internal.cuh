@@ -151,10 +151,12 @@ struct Plan {
 struct Table {
   Ctx* ctx = nullptr;
   int scheme = 1, K = 1;
-  int64_t G = 0;
+  int64_t G = 0;              // bins of this table (a shard: layers [slab_lo, slab_hi))
+  int64_t bin0 = 0;           // global index of the first bin (location-grid shard)
+  int slab_lo = 0, slab_hi = 0;  // layer range along z (3-D) or y (2-D)
   int P = 0, N = 0, os = 1, M = 0;
   double scale = 0.0;
-  gh_grid grid{};
+  gh_grid grid{};             // the FULL grid: points stay bit-identical
   std::vector<double> tx, rx;
   double* txrx_d = nullptr;   // [P][6] tx xyz, rx xyz
   uint32_t* idx_d = nullptr;  // [G][P][K]
@@ -224,7 +226,8 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
                    float* map_d, unsigned long long* keys_d);
 void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
                         int64_t* idx_d, float* val_d);
-void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t* idx_d,
+void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
+                 int64_t* idx_d,
                  float* val_d);
 void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const float2* frames_d, int T, int combine, float* map_d,

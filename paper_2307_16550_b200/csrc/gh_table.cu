@@ -200,7 +200,7 @@ struct BuildArgs {
   const double* txrx;  // [P][6]
   double scale;
   int P, N, os, K, scheme, wrap;
-  int64_t G;
+  int64_t G, bin0;     // local bins, global index of the first
   uint32_t* idx;
   double2* coef;
   uint8_t* flags;      // window (1) / degenerate (2) per entry
@@ -216,7 +216,7 @@ __global__ void k_build(BuildArgs a) {
     const int64_t b = e / a.P;
     const int p = (int)(e % a.P);
     double x[3];
-    dgrid_point(a.grid, b, x);
+    dgrid_point(a.grid, a.bin0 + b, x);
     const double* tx = a.txrx + 6 * p;
     const double dtx = dnorm3(tx, x[0], x[1], x[2]);
     const double drx = dnorm3(tx + 3, x[0], x[1], x[2]);
@@ -231,7 +231,7 @@ __global__ void k_build(BuildArgs a) {
     const double res = fit_atom(a.N, a.os, r, a.scheme, idx, c);
     for (int j = 0; j < a.K; ++j) {
       a.idx[e * a.K + j] = idx[j];
-      a.coef[e * a.K + j] = make_double2(c[j].re, c[j].im);
+      if (a.coef) a.coef[e * a.K + j] = make_double2(c[j].re, c[j].im);
     }
     worst = fmax(worst, res);
   }
@@ -304,7 +304,7 @@ struct FillArgs {
   const uint32_t* idx;    // [G][P][K]
   const double2* coef;
   int P, K, M, p4, k3, lanes;
-  int64_t G;
+  int64_t G, bin0;        // local bins; tiles carry global coordinates
   uint16_t* rows;
   float2* coef3;
   int* err;
@@ -327,8 +327,11 @@ __global__ void k_fill_plan(FillArgs a) {
   for (int64_t e = start; e < total; e += step) {
     const int64_t lb = e / a.P;
     const int p = (int)(e % a.P);
-    int64_t gb = entry0 + lb;
-    if (a.tiles) tile_bin(td, a.grid, lb, &gb);
+    int64_t gb = entry0 + lb;  // local bin
+    if (a.tiles) {
+      tile_bin(td, a.grid, lb, &gb);  // global bin
+      gb -= a.bin0;
+    }
     const int4 w = win[p];
     const int64_t at = (gb * a.P + p) * a.K;
     const int first = (int)a.idx[at];
@@ -356,7 +359,8 @@ constexpr size_t kStageBudget = 216 * 1024;
 void build_table_device(Ctx* ctx, Table* t, int wrap) {
   const int64_t total = t->G * t->P;
   GH_CUDA(cudaMalloc(&t->idx_d, sizeof(uint32_t) * total * t->K));
-  GH_CUDA(cudaMalloc(&t->coef_d, sizeof(double2) * total * t->K));
+  // nearest (K = 1) coefficients are identically 1: not stored
+  if (t->K > 1) GH_CUDA(cudaMalloc(&t->coef_d, sizeof(double2) * total * t->K));
   uint8_t* flags = nullptr;
   unsigned long long* scal = nullptr;  // [0] max residual bits, [1] flag count, [2] next flag
   GH_CUDA(cudaMalloc(&flags, total));
@@ -373,6 +377,7 @@ void build_table_device(Ctx* ctx, Table* t, int wrap) {
   a.scheme = t->scheme;
   a.wrap = wrap;
   a.G = t->G;
+  a.bin0 = t->bin0;
   a.idx = t->idx_d;
   a.coef = t->coef_d;
   a.flags = flags;
@@ -409,7 +414,7 @@ void build_table_device(Ctx* ctx, Table* t, int wrap) {
       if (fl & 2) degenerate = true;
       char buf[64];
       std::snprintf(buf, sizeof buf, "%s(bin %lld, rx %d)", names.empty() ? "" : ", ",
-                    (long long)(nx / t->P), (int)(nx % t->P));
+                    (long long)(t->bin0 + nx / t->P), (int)(nx % t->P));
       names += buf;
       after = (int64_t)nx;
     }
@@ -456,7 +461,14 @@ void build_plan(Ctx* ctx, Table* t) {
     GH_CUDA(cudaStreamSynchronize(ctx->stream));
   } else {
     pl.full = false;
+    // trial batch: the widest of 32 / 16 / 8 trials (power) or 16 / 8
+    // (complex) that still leaves >= 40 staged rows per pair — 128-byte rows
+    // are bank-conflict free, narrower rows trade conflicts for tile size
+    // when there are many pairs (BASELINE c5: 64)
     pl.tb = pl.k3 ? 16 : 32;
+    while (pl.tb > 8 &&
+           static_cast<int>(kStageBudget / (static_cast<size_t>(pl.tb) * pl.esize)) / P < 40)
+      pl.tb >>= 1;
     const int budget_rows = static_cast<int>(kStageBudget / (static_cast<size_t>(pl.tb) * pl.esize));
     const int allow = budget_rows / P - 5;
     if (allow < 4) fail(GH_EINVAL, "gather plan: too many pairs for one shared-memory window");
@@ -483,17 +495,20 @@ void build_plan(Ctx* ctx, Table* t) {
         w[d] = std::min(w[d], g.n[d]);
       }
       if (dims == 2) w[2] = 1;
+      // the shard's box: layers [slab_lo, slab_hi) of z (3-D) or y (2-D)
+      const int z_lo = dims == 3 ? t->slab_lo : 0, z_hi = dims == 3 ? t->slab_hi : g.n[2];
+      const int y_lo = dims == 3 ? 0 : t->slab_lo, y_hi = dims == 3 ? g.n[1] : t->slab_hi;
       int64_t off = 0;
-      for (int z = 0; z < g.n[2]; z += w[2])
-        for (int y = 0; y < g.n[1]; y += w[1])
+      for (int z = z_lo; z < z_hi; z += w[2])
+        for (int y = y_lo; y < y_hi; y += w[1])
           for (int x = 0; x < g.n[0]; x += w[0]) {
             TileDesc td{};
             td.x0 = x;
             td.y0 = y;
             td.z0 = z;
             td.wx = std::min(w[0], g.n[0] - x);
-            td.wy = std::min(w[1], g.n[1] - y);
-            td.wz = std::min(w[2], g.n[2] - z);
+            td.wy = std::min(w[1], y_hi - y);
+            td.wz = std::min(w[2], z_hi - z);
             td.entry_off = off;
             off += (int64_t)td.wx * td.wy * td.wz;
             tl.tiles.push_back(td);
@@ -587,6 +602,7 @@ void build_plan(Ctx* ctx, Table* t) {
   f.k3 = pl.k3;
   f.lanes = pl.tb * pl.esize / 16;
   f.G = t->G;
+  f.bin0 = t->bin0;
   f.rows = pl.rows_d;
   f.coef3 = pl.coef3_d;
   f.err = err_d;

@@ -27,7 +27,7 @@ __device__ __forceinline__ bool better(float v, int64_t i, float bv, int64_t bi)
 
 __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __restrict__ map,
                                                                int64_t G, int nx, int ny, int nz,
-                                                               int K, int64_t* idx_out,
+                                                               int K, int64_t bin0, int64_t* idx_out,
                                                                float* val_out) {
   const int trial = blockIdx.x;
   const float* m = map + (int64_t)trial * G;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
           bw = sw[w];
         }
       const bool valid = bi != INT64_MAX && bv != -INFINITY;
-      idx_out[(int64_t)trial * K + k] = valid ? bi : -1;
+      idx_out[(int64_t)trial * K + k] = valid ? bin0 + bi : -1;
       val_out[(int64_t)trial * K + k] = valid ? bv : 0.0f;
       winner = valid ? bw : -1;
     }
@@ -144,12 +144,13 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
 
 }  // namespace
 
-void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t* idx_d,
+void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
+                 int64_t* idx_d,
                  float* val_d) {
   if (K < 1 || K > kMaxK) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
   const int64_t G = (int64_t)g.n[0] * g.n[1] * g.n[2];
   KTimer kt(ctx, "topk");
-  k_topk_localmax<<<T, kTopkThreads, 0, ctx->stream>>>(map_d, G, g.n[0], g.n[1], g.n[2], K, idx_d,
+  k_topk_localmax<<<T, kTopkThreads, 0, ctx->stream>>>(map_d, G, g.n[0], g.n[1], g.n[2], K, bin0, idx_d,
                                                        val_d);
   GH_LAUNCHED(ctx);
 }

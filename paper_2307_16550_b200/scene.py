@@ -199,6 +199,15 @@ class Scene:
         """Gather units (bin x pair correlations) per trial, SURVEY §8(d)."""
         return self.n_bins * self.n_pairs
 
+    def slab_axis_len(self) -> int:
+        """Length of the axis location-grid shards split: z (3-D) or y (2-D)."""
+        return int(self.grid_n[2]) if int(self.grid_n[2]) > 1 else int(self.grid_n[1])
+
+    def slab_bins(self, lo: int, hi: int) -> tuple[int, int]:
+        """Global bin range [b0, b1) of layers [lo, hi) (contiguous, x fastest)."""
+        layer = int(self.grid_n[0]) * (int(self.grid_n[1]) if int(self.grid_n[2]) > 1 else 1)
+        return lo * layer, hi * layer
+
 
 def _circle(radius: float, angles_deg) -> np.ndarray:
     a = np.deg2rad(np.asarray(angles_deg, dtype=np.float64))

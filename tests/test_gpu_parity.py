@@ -299,3 +299,43 @@ def test_campaign_statistics_match_oracle(ctx):
         so = D.campaign_stats(sc, o_idx, truth)
         sg = D.campaign_stats(sc, g_idx.cpu().numpy(), truth)
         assert np.allclose(so, sg), (snr, so, sg)
+
+
+def c5_reduced():
+    # BASELINE c5 stations/waveform (64 pairs, N = 512, os = 4, 3-D grid
+    # spacing 0.195 x 0.195 x 0.3125 m) on a 48 x 40 x 8 block of the grid
+    c5 = S.baseline("c5")
+    sx, sz = c5.grid_spacing[0], c5.grid_spacing[2]
+    return c5.with_(grid_n=(48, 40, 8), grid_origin=(-4.7, -3.9, 8.0 + sz / 2),
+                    area_lo=(-4.8, -4.0, 8.0), area_hi=(-4.8 + 48 * sx, -4.0 + 40 * sx, 8.0 + 8 * sz))
+
+
+def test_c5_geometry_3d_and_grid_sharding(ctx):
+    from paper_2307_16550_b200 import distributed as D
+    sc = c5_reduced()
+    T = 24
+    oi, oc, _ = O.build_table(sc)
+    full = gh.precompute_hop_table(ctx, sc)
+    gi_, _ = full.download()
+    assert np.array_equal(gi_, oi)
+    fr, _ = O.synth(sc, 0, T)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, full, fd).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    g_idx, _ = gh.hop_argmax(ctx, full, fd)
+    assert_argmax_parity(ref, g_idx.cpu().numpy(), "c5 reduced")
+    # two location-grid shards (z layers 0-3 and 3-8): shard rows equal the
+    # full table, and merging shard winners by key == the full argmax
+    keys = np.zeros(T, dtype=np.int64)
+    for lo, hi in ((0, 3), (3, 8)):
+        sh = gh.precompute_hop_table_shard(ctx, sc, lo, hi)
+        b0, b1 = sc.slab_bins(lo, hi)
+        si, _ = sh.download()
+        assert np.array_equal(si, oi[b0:b1])
+        sm_ = gh.hop_decision_map(ctx, sh, fd).cpu().numpy()
+        assert np.abs(sm_ - m[:, b0:b1]).max() <= 1e-6 * np.abs(m).max()
+        ix, vx = gh.hop_argmax(ctx, sh, fd)
+        keys = np.maximum(keys, D.encode_keys(vx.cpu().numpy(), ix.cpu().numpy()))
+    bins, _ = D.decode_keys(keys)
+    assert np.array_equal(bins, g_idx.cpu().numpy())
