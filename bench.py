@@ -295,7 +295,7 @@ def run_ours(args, world, rank, local):
 
     # ---- direct method (BASELINE c2 "run both ways"): tcgen05 3xTF32
     direct = None
-    if not args.no_direct:
+    if not args.no_direct and sc.name in ("c1", "c2"):
         for _ in range(2):
             gh.direct_argmax(ctx, sc, frames)
         ctx.synchronize()
@@ -334,16 +334,19 @@ def run_ours(args, world, rank, local):
         return
     pk = peaks()
     g_avg = g_ms / max(g_n, 1)
-    lsu_bytes = T * G * P * 4.0  # fp32 power gathered per (trial, bin, pair)
+    # shared-memory bytes gathered per unit: fp32 power (K = 1) or three
+    # complex64 spectrum values (K = 3)
+    lsu_bytes = T * G * P * (4.0 if sc.k == 1 else 24.0)
     achieved = lsu_bytes / (g_avg * 1e-3) / 1e9
     hbm_bytes = T * P * sc.n_fft * 4.0 + G * 4 * 2  # staged spectra + table rows
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic (counter-based RNG, seed 20260816), c2 scene",
+        "data": f"synthetic (counter-based RNG, seed 20260816), {sc.name} scene",
         "config": {"workload": f"{sc.name}: {T} trials/GPU, {G} bins x {P} pairs, N={N}, "
-                               f"M={sc.n_fft}, nearest (K=1), power sum, wrap mode",
+                               f"M={sc.n_fft}, {S.SCHEME_NAMES[sc.scheme]} (K={sc.k}), power sum, "
+                               f"{'wrap mode' if sc.wrap else 'reference window check'}",
                    "trials_per_gpu": T, "bins": G, "pairs": P, "n_fft": sc.n_fft,
                    "l2": "flushed between timed steps (512 MB write, outside the events)",
                    "parallelism": f"trial-sharded x{world}"},
@@ -352,7 +355,7 @@ def run_ours(args, world, rank, local):
         "kernels_ms": {"fft": f_ms / max(f_n, 1), "gather": g_avg, "decode": d_ms / max(d_n, 1)},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": None,
-                     "kernel": "k_gather<16,false,false,false>",
+                     "kernel": "k_gather (fused argmax)",
                      "peak_source": "measured in-run (gh_measure_smem_peak, LDS.128 all SMs)",
                      "algorithmic_bytes_per_launch": lsu_bytes,
                      "hbm": {"bytes_per_launch": hbm_bytes,
@@ -378,6 +381,79 @@ def run_ours(args, world, rank, local):
         tdist.destroy_process_group()
 
 
+def run_grid_sharded(args, world, rank, local):
+    """BASELINE c5: the location grid is sharded across ranks (z layers);
+    every rank synthesises the same trials (no signal traffic) and scans its
+    slab; per-trial winners merge with one NCCL all-reduce(MAX) of the int64
+    key (value bits << 32 | 2^32-1-bin). value = full-grid units / step."""
+    import torch
+    import paper_2307_16550_b200 as gh
+    from paper_2307_16550_b200 import distributed as D
+    from paper_2307_16550_b200 import scene as S
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    sc = S.baseline(args.config)
+    T = args.trials or 256
+    lo, hi = D.shard(sc.slab_axis_len(), world, rank)
+    ctx = gh.Context(local)
+    t_build = time.perf_counter()
+    table = gh.precompute_hop_table_shard(ctx, sc, lo, hi)
+    ctx.synchronize()
+    t_build = time.perf_counter() - t_build
+    dev = f"cuda:{local}"
+    idx = torch.empty(T, dtype=torch.int64, device=dev)
+    val = torch.empty(T, dtype=torch.float32, device=dev)
+    keys = torch.empty(T, dtype=torch.int64, device=dev)
+
+    def step(k):
+        gh.campaign_hop(ctx, table, sc, k * T, T, out=(idx, val))
+        # key = float bits << 32 | (2^32 - 1 - bin), merged across shards
+        kk = (val.view(torch.int32).to(torch.int64) << 32) | (0xFFFFFFFF - idx)
+        keys.copy_(kk)
+        if dist:
+            tdist.all_reduce(keys, op=tdist.ReduceOp.MAX)
+        return keys
+
+    for k in range(max(3, args.warmup)):
+        step(k)
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for k in range(args.steps):
+            step(k)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = D.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
+    if dist:
+        tdist.barrier()
+    if rank == 0:
+        units = T * sc.units_per_trial()
+        line = {
+            "metric": METRIC, "value": units / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "data": f"synthetic (counter-based RNG, seed 20260816), {sc.name} scene",
+            "config": {"workload": f"{sc.name}: {T} trials/step, {sc.n_bins} bins x {sc.n_pairs} "
+                                   f"pairs, N={sc.n_samples}, M={sc.n_fft}, location grid sharded "
+                                   f"over {world} GPU(s) ({sc.slab_axis_len()} z layers)",
+                       "trials_per_step": T, "bins": sc.n_bins, "pairs": sc.n_pairs,
+                       "parallelism": f"grid-sharded x{world}"},
+            "trials_per_s": T / (ms * 1e-3),
+            "table_build_s_rank0": t_build,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -394,6 +470,8 @@ def main():
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.config == "c5":
+        run_grid_sharded(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -113,19 +113,22 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   __shared__ float red_v[NW * TB];
   __shared__ int red_i[NW * TB];
 
-  const int tb = blockIdx.x;
+  // grid: x = location tile / bin chunk (fastest: every tile of a trial
+  // batch runs together, so the batch's spectra stay L2-resident), y = batch
+  const int tb = blockIdx.y;
+  const int64_t col = blockIdx.x;
   int64_t entry0, nb;
   TileDesc td{};
   const int4* win;
   if (a.full) {
-    entry0 = (int64_t)blockIdx.y * a.chunk_bins;
+    entry0 = col * a.chunk_bins;
     nb = a.G - entry0 < a.chunk_bins ? a.G - entry0 : a.chunk_bins;
     win = a.win;
   } else {
-    td = a.tiles[blockIdx.y];
+    td = a.tiles[col];
     entry0 = td.entry_off;
     nb = (int64_t)td.wx * td.wy * td.wz;
-    win = a.win + (int64_t)blockIdx.y * a.P;
+    win = a.win + col * a.P;
   }
   const int P = PC ? PC : a.P;
 
@@ -361,9 +364,9 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
     a.chunk_bins = (t->G + chunks - 1) / chunks;
     n_cols = static_cast<int>((t->G + a.chunk_bins - 1) / a.chunk_bins);
   }
-  if (n_cols > 65535) fail(GH_EINVAL, "gather: too many location tiles for one launch");
+  if (n_tb > 65535) fail(GH_EINVAL, "gather: too many trial batches for one launch");
   const size_t smem = static_cast<size_t>(pl.max_rows) * pl.tb * pl.esize;
-  dim3 grid(n_tb, n_cols);
+  dim3 grid(n_cols, n_tb);
   const bool mag = combine == GH_MAGNITUDE;
   const bool mapmode = map_d != nullptr;
   if (!pl.k3) {
