@@ -112,6 +112,7 @@ void free_table(gh::Table* t) {
   cudaFree(t->plan.win_d);
   cudaFree(t->plan.rows_d);
   cudaFree(t->plan.coef3_d);
+  cudaFree(t->plan.binid_d);
   delete t;
 }
 

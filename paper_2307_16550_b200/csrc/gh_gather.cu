@@ -41,6 +41,7 @@ struct GatherArgs {
   const int4* win;        // [tiles][P] / [P]
   const uint16_t* rows;   // [entries][p4], 16-byte units
   const float2* coef3;    // [entries][P][3]
+  const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
   gh_grid grid;
   int64_t G;              // bins of the table (shard)
   int64_t bin0;           // global index of the shard's first bin
@@ -53,9 +54,16 @@ struct GatherArgs {
 
 __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDesc& td,
                                               int64_t entry0, int64_t lb) {
-  if (a.full) return a.bin0 + entry0 + lb;
+  if (a.full) return a.binid ? (int64_t)__ldg(a.binid + entry0 + lb) : a.bin0 + entry0 + lb;
   const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
+}
+
+// tie rule between two entries of one CTA: smaller global bin. Entry order is
+// bin order except in bank-permuted plans, where the bin ids decide.
+__device__ __forceinline__ bool entry_before(const GatherArgs& a, int64_t entry0, int x, int y) {
+  if (a.binid) return __ldg(a.binid + entry0 + x) < __ldg(a.binid + entry0 + y);
+  return x < y;
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
@@ -101,7 +109,7 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
 }
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool PERM>
 __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a) {
   constexpr int kGatherThreads = gather_threads<K3>();
   constexpr int ES = K3 ? 8 : 4;         // staged element bytes
@@ -167,20 +175,28 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint2 cur[PQ], nxt[PQ];
+  unsigned cur_bid = 0, nxt_bid = 0;         // permuted plans: bin of block entry `lane`
+  unsigned long long bestk[TPL];             // permuted plans: best key per trial
+#pragma unroll
+  for (int i = 0; i < TPL; ++i) bestk[i] = 0ull;
 #pragma unroll
   for (int q = 0; q < PQ; ++q) {
     cur[q] = make_uint2(0u, 0u);
     nxt[q] = make_uint2(0u, 0u);
   }
-  if (w0 + lane < w1)
+  if (w0 + lane < w1) {
 #pragma unroll
     for (int q = 0; q < PQ; ++q)
       if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
+    if constexpr (PERM) cur_bid = __ldg(a.binid + entry0 + w0 + lane);
+  }
   for (int64_t blk = w0; blk < w1; blk += 32) {
-    if (blk + 32 + lane < w1)
+    if (blk + 32 + lane < w1) {
 #pragma unroll
       for (int q = 0; q < PQ; ++q)
         if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
+      if constexpr (PERM) nxt_bid = __ldg(a.binid + entry0 + blk + 32 + lane);
+    }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
     // one step: lane group `sub` handles bin j = s * BPW + sub of the block
     auto step = [&](int s, bool check) {
@@ -212,6 +228,8 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
         vals[0] = acc[0].x;
         vals[1] = acc[0].y;
       }
+      unsigned low = 0;  // ~bin of this lane group's entry (permuted plans), all lanes
+      if constexpr (PERM) low = 0xffffffffu - __shfl_sync(0xffffffffu, cur_bid, j & 31);
       if (!check || j < nblk) {
         if constexpr (MAPMODE) {
           const int64_t gb = global_bin(a, td, entry0, lb);
@@ -223,10 +241,25 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
         } else {
 #pragma unroll
           for (int i = 0; i < TPL; ++i)
-            if (vals[i] > best[i]) {
-              best[i] = vals[i];
-              blb[i] = (int)lb;
+          {
+            if constexpr (PERM) {
+              // permuted entries: the 64-bit key (value bits, ~bin) carries
+              // the tie rule, no branches
+#pragma unroll
+              for (int i = 0; i < TPL; ++i) {
+                const unsigned long long k =
+                    ((unsigned long long)__float_as_uint(vals[i]) << 32) | low;
+                bestk[i] = k > bestk[i] ? k : bestk[i];
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < TPL; ++i)
+                if (vals[i] > best[i]) {
+                  best[i] = vals[i];
+                  blb[i] = (int)lb;
+                }
             }
+          }
         }
       }
     };
@@ -244,8 +277,30 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
     }
 #pragma unroll
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
+    cur_bid = nxt_bid;
   }
-  if constexpr (!MAPMODE) {
+  if constexpr (!MAPMODE && PERM) {
+    __shared__ unsigned long long red_k[NW * TB];
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) {
+      for (int o = L; o < 32; o <<= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bestk[i], o);
+        bestk[i] = ok > bestk[i] ? ok : bestk[i];
+      }
+      if (sub == 0) red_k[warp * TB + v * TPL + i] = bestk[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < TB) {
+      unsigned long long bk = 0ull;
+      for (int w = 0; w < NW; ++w) {
+        const unsigned long long k = red_k[w * TB + threadIdx.x];
+        bk = k > bk ? k : bk;
+      }
+      const int trial = tb * TB + threadIdx.x;
+      if (trial < a.T && bk) atomicMax(a.keys + trial, bk);
+    }
+  }
+  if constexpr (!MAPMODE && !PERM) {
     // merge the BPW lane groups of the warp (same trials, different bins)
 #pragma unroll
     for (int i = 0; i < TPL; ++i) {
@@ -298,9 +353,9 @@ __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* id
   val[t] = __uint_as_float((unsigned)(k >> 32));
 }
 
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool PERM = false>
 void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ>;
+  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ, PERM>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   KTimer kt(ctx, "gather");
@@ -313,6 +368,15 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
 template <int TB, bool K3, bool MAG, bool MAPMODE>
 void dispatch_p(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   const int pq = a.p4 / 4;
+  if constexpr (TB == 16 && !K3 && !MAPMODE) {
+    // bank-permuted full-ring plan (P <= 8): key-based argmax
+    if (a.binid) {
+      if (a.P == 3) run<TB, K3, MAG, MAPMODE, 3, 1, true>(ctx, a, grid, smem);
+      else if (pq <= 1) run<TB, K3, MAG, MAPMODE, 0, 1, true>(ctx, a, grid, smem);
+      else run<TB, K3, MAG, MAPMODE, 0, 4, true>(ctx, a, grid, smem);
+      return;
+    }
+  }
   if (a.P == 3) run<TB, K3, MAG, MAPMODE, 3, 1>(ctx, a, grid, smem);
   else if (a.P == 16) run<TB, K3, MAG, MAPMODE, 16, 4>(ctx, a, grid, smem);
   else if (a.P == 64) run<TB, K3, MAG, MAPMODE, 64, 16>(ctx, a, grid, smem);
@@ -344,6 +408,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.win = pl.win_d;
   a.rows = pl.rows_d;
   a.coef3 = pl.coef3_d;
+  a.binid = pl.full ? pl.binid_d : nullptr;
   a.grid = t->grid;
   a.G = t->G;
   a.bin0 = t->bin0;
@@ -361,7 +426,8 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
     // per CTA to amortise the staging of the whole ring
     int64_t chunks = (2LL * ctx->num_sms + n_tb - 1) / n_tb;
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (t->G + 4095) / 4096));
-    a.chunk_bins = (t->G + chunks - 1) / chunks;
+    // multiple of 32: bank-complementary entry pairs stay on even offsets
+    a.chunk_bins = ((t->G + chunks - 1) / chunks + 31) / 32 * 32;
     n_cols = static_cast<int>((t->G + a.chunk_bins - 1) / a.chunk_bins);
   }
   if (n_tb > 65535) fail(GH_EINVAL, "gather: too many trial batches for one launch");

@@ -145,6 +145,7 @@ struct Plan {
   int4* win_d = nullptr;         // [tiles][P] {base, len, row_start, 0}
   uint16_t* rows_d = nullptr;    // [entries][p4] first staged row per pair
   float2* coef3_d = nullptr;     // [entries][P][3] (k3 only)
+  uint32_t* binid_d = nullptr;   // [entries] global bin of each entry (permuted plans)
   int64_t n_entries = 0;
 };
 

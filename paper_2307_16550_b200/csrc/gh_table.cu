@@ -354,6 +354,68 @@ __global__ void k_fill_plan(FillArgs a) {
 
 constexpr size_t kStageBudget = 216 * 1024;
 
+// Bank-conflict-aware bin order for the 16-trial full-ring power plan. A row
+// there is 64 bytes (half a shared-memory wavefront) and the gather serves
+// two bins per quarter-warp with one LDS.128 per pair: the two rows collide
+// when their row indices have equal parity. Bins are re-ordered so that
+// entries (2k, 2k+1) have complementary parity vectors over the pairs
+// wherever possible (greedy matching of vector v with ~v within windows of
+// 1024 bins); `binid` maps entries back to bins, which keeps reported
+// indices and the smallest-bin tie rule exact.
+void permute_for_banks(Ctx* ctx, Table* t) {
+  Plan& pl = t->plan;
+  const int P = t->P, p4 = pl.p4, L = pl.tb * pl.esize / 16;
+  const int64_t n = pl.n_entries;
+  std::vector<uint16_t> rows(static_cast<size_t>(n) * p4);
+  GH_CUDA(cudaMemcpyAsync(rows.data(), pl.rows_d, sizeof(uint16_t) * rows.size(),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  const unsigned full = (1u << P) - 1u;
+  std::vector<uint32_t> order;
+  order.reserve(static_cast<size_t>(n));
+  constexpr int64_t W = 1024;
+  std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
+  for (int64_t w0 = 0; w0 < n; w0 += W) {
+    const int64_t w1 = std::min<int64_t>(n, w0 + W);
+    for (auto& b : bucket) b.clear();
+    for (int64_t e = w1 - 1; e >= w0; --e) {  // reversed: pop_back yields ascending
+      unsigned v = 0;
+      for (int p = 0; p < P; ++p) v |= ((rows[e * p4 + p] / L) & 1u) << p;
+      bucket[v].push_back(static_cast<uint32_t>(e));
+    }
+    std::vector<uint32_t> rest;
+    for (unsigned v = 0; v <= full; ++v) {
+      auto& a = bucket[v];
+      auto& b = bucket[full ^ v];
+      if (v > (full ^ v)) continue;  // each complementary couple once
+      while (!a.empty() && !b.empty() && (&a != &b || a.size() >= 2)) {
+        order.push_back(a.back());
+        a.pop_back();
+        order.push_back(b.back());
+        b.pop_back();
+      }
+    }
+    for (auto& b : bucket)
+      for (auto it = b.rbegin(); it != b.rend(); ++it) rest.push_back(*it);
+    std::sort(rest.begin(), rest.end());
+    order.insert(order.end(), rest.begin(), rest.end());
+  }
+  std::vector<uint16_t> prow(rows.size());
+  std::vector<uint32_t> binid(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t e = order[static_cast<size_t>(i)];
+    std::memcpy(&prow[static_cast<size_t>(i) * p4], &rows[static_cast<size_t>(e) * p4],
+                sizeof(uint16_t) * p4);
+    binid[static_cast<size_t>(i)] = static_cast<uint32_t>(t->bin0 + e);
+  }
+  GH_CUDA(cudaMemcpyAsync(pl.rows_d, prow.data(), sizeof(uint16_t) * prow.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  GH_CUDA(cudaMalloc(&pl.binid_d, sizeof(uint32_t) * n));
+  GH_CUDA(cudaMemcpyAsync(pl.binid_d, binid.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 }  // namespace
 
 void build_table_device(Ctx* ctx, Table* t, int wrap) {
@@ -618,6 +680,7 @@ void build_plan(Ctx* ctx, Table* t) {
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(err_d);
   if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
+  if (pl.full && !pl.k3 && P <= 8) permute_for_banks(ctx, t);
   pl.built = true;
 }
 
