@@ -109,7 +109,7 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
 }
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool PERM>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
 __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a) {
   constexpr int kGatherThreads = gather_threads<K3>();
   constexpr int ES = K3 ? 8 : 4;         // staged element bytes
@@ -175,10 +175,6 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint2 cur[PQ], nxt[PQ];
-  unsigned cur_bid = 0, nxt_bid = 0;         // permuted plans: bin of block entry `lane`
-  unsigned long long bestk[TPL];             // permuted plans: best key per trial
-#pragma unroll
-  for (int i = 0; i < TPL; ++i) bestk[i] = 0ull;
 #pragma unroll
   for (int q = 0; q < PQ; ++q) {
     cur[q] = make_uint2(0u, 0u);
@@ -188,14 +184,12 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
 #pragma unroll
     for (int q = 0; q < PQ; ++q)
       if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
-    if constexpr (PERM) cur_bid = __ldg(a.binid + entry0 + w0 + lane);
   }
   for (int64_t blk = w0; blk < w1; blk += 32) {
     if (blk + 32 + lane < w1) {
 #pragma unroll
       for (int q = 0; q < PQ; ++q)
         if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
-      if constexpr (PERM) nxt_bid = __ldg(a.binid + entry0 + blk + 32 + lane);
     }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
     // one step: lane group `sub` handles bin j = s * BPW + sub of the block
@@ -228,8 +222,6 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
         vals[0] = acc[0].x;
         vals[1] = acc[0].y;
       }
-      unsigned low = 0;  // ~bin of this lane group's entry (permuted plans), all lanes
-      if constexpr (PERM) low = 0xffffffffu - __shfl_sync(0xffffffffu, cur_bid, j & 31);
       if (!check || j < nblk) {
         if constexpr (MAPMODE) {
           const int64_t gb = global_bin(a, td, entry0, lb);
@@ -241,25 +233,10 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
         } else {
 #pragma unroll
           for (int i = 0; i < TPL; ++i)
-          {
-            if constexpr (PERM) {
-              // permuted entries: the 64-bit key (value bits, ~bin) carries
-              // the tie rule, no branches
-#pragma unroll
-              for (int i = 0; i < TPL; ++i) {
-                const unsigned long long k =
-                    ((unsigned long long)__float_as_uint(vals[i]) << 32) | low;
-                bestk[i] = k > bestk[i] ? k : bestk[i];
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < TPL; ++i)
-                if (vals[i] > best[i]) {
-                  best[i] = vals[i];
-                  blb[i] = (int)lb;
-                }
+            if (vals[i] > best[i]) {
+              best[i] = vals[i];
+              blb[i] = (int)lb;
             }
-          }
         }
       }
     };
@@ -277,30 +254,8 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
     }
 #pragma unroll
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
-    cur_bid = nxt_bid;
   }
-  if constexpr (!MAPMODE && PERM) {
-    __shared__ unsigned long long red_k[NW * TB];
-#pragma unroll
-    for (int i = 0; i < TPL; ++i) {
-      for (int o = L; o < 32; o <<= 1) {
-        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, bestk[i], o);
-        bestk[i] = ok > bestk[i] ? ok : bestk[i];
-      }
-      if (sub == 0) red_k[warp * TB + v * TPL + i] = bestk[i];
-    }
-    __syncthreads();
-    if (threadIdx.x < TB) {
-      unsigned long long bk = 0ull;
-      for (int w = 0; w < NW; ++w) {
-        const unsigned long long k = red_k[w * TB + threadIdx.x];
-        bk = k > bk ? k : bk;
-      }
-      const int trial = tb * TB + threadIdx.x;
-      if (trial < a.T && bk) atomicMax(a.keys + trial, bk);
-    }
-  }
-  if constexpr (!MAPMODE && !PERM) {
+  if constexpr (!MAPMODE) {
     // merge the BPW lane groups of the warp (same trials, different bins)
 #pragma unroll
     for (int i = 0; i < TPL; ++i) {
@@ -353,9 +308,9 @@ __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* id
   val[t] = __uint_as_float((unsigned)(k >> 32));
 }
 
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool PERM = false>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
 void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ, PERM>;
+  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   KTimer kt(ctx, "gather");
@@ -368,15 +323,6 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
 template <int TB, bool K3, bool MAG, bool MAPMODE>
 void dispatch_p(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   const int pq = a.p4 / 4;
-  if constexpr (TB == 16 && !K3 && !MAPMODE) {
-    // bank-permuted full-ring plan (P <= 8): key-based argmax
-    if (a.binid) {
-      if (a.P == 3) run<TB, K3, MAG, MAPMODE, 3, 1, true>(ctx, a, grid, smem);
-      else if (pq <= 1) run<TB, K3, MAG, MAPMODE, 0, 1, true>(ctx, a, grid, smem);
-      else run<TB, K3, MAG, MAPMODE, 0, 4, true>(ctx, a, grid, smem);
-      return;
-    }
-  }
   if (a.P == 3) run<TB, K3, MAG, MAPMODE, 3, 1>(ctx, a, grid, smem);
   else if (a.P == 16) run<TB, K3, MAG, MAPMODE, 16, 4>(ctx, a, grid, smem);
   else if (a.P == 64) run<TB, K3, MAG, MAPMODE, 64, 16>(ctx, a, grid, smem);

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <unordered_map>
 
 #include "gh_internal.cuh"
 
@@ -371,17 +372,40 @@ void permute_for_banks(Ctx* ctx, Table* t) {
                           cudaMemcpyDeviceToHost, ctx->stream));
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
   const unsigned full = (1u << P) - 1u;
+  // Bins whose rows equal an earlier bin's for every pair always tie with
+  // it and can never win the argmax: they go last (ascending), so entry
+  // order still resolves every forced tie to the smallest bin and the
+  // gather keeps its branch-free "first strict maximum" update.
+  std::vector<uint32_t> uniq, dups;
+  {
+    std::unordered_map<uint64_t, uint32_t> seen;
+    seen.reserve(static_cast<size_t>(n) * 2);
+    for (int64_t e = 0; e < n; ++e) {
+      uint64_t h = 0;
+      for (int p = 0; p < p4; ++p) h = (h << 16) ^ rows[e * p4 + p] ^ (h >> 48);
+      bool dup = false;
+      auto it = seen.find(h);
+      if (it != seen.end())
+        dup = std::memcmp(&rows[e * p4], &rows[static_cast<size_t>(it->second) * p4],
+                          sizeof(uint16_t) * p4) == 0;
+      else
+        seen.emplace(h, static_cast<uint32_t>(e));
+      (dup ? dups : uniq).push_back(static_cast<uint32_t>(e));
+    }
+  }
   std::vector<uint32_t> order;
   order.reserve(static_cast<size_t>(n));
-  constexpr int64_t W = 1024;
+  constexpr int64_t W = 1024;  // even: pairs stay on even entry offsets
   std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
-  for (int64_t w0 = 0; w0 < n; w0 += W) {
-    const int64_t w1 = std::min<int64_t>(n, w0 + W);
+  const int64_t nu = static_cast<int64_t>(uniq.size());
+  for (int64_t w0 = 0; w0 < nu; w0 += W) {
+    const int64_t w1 = std::min<int64_t>(nu, w0 + W);
     for (auto& b : bucket) b.clear();
-    for (int64_t e = w1 - 1; e >= w0; --e) {  // reversed: pop_back yields ascending
+    for (int64_t u = w1 - 1; u >= w0; --u) {  // reversed: pop_back yields ascending
+      const uint32_t e = uniq[static_cast<size_t>(u)];
       unsigned v = 0;
-      for (int p = 0; p < P; ++p) v |= ((rows[e * p4 + p] / L) & 1u) << p;
-      bucket[v].push_back(static_cast<uint32_t>(e));
+      for (int p = 0; p < P; ++p) v |= ((rows[static_cast<size_t>(e) * p4 + p] / L) & 1u) << p;
+      bucket[v].push_back(e);
     }
     std::vector<uint32_t> rest;
     for (unsigned v = 0; v <= full; ++v) {
@@ -400,6 +424,7 @@ void permute_for_banks(Ctx* ctx, Table* t) {
     std::sort(rest.begin(), rest.end());
     order.insert(order.end(), rest.begin(), rest.end());
   }
+  order.insert(order.end(), dups.begin(), dups.end());
   std::vector<uint16_t> prow(rows.size());
   std::vector<uint32_t> binid(static_cast<size_t>(n));
   for (int64_t i = 0; i < n; ++i) {
