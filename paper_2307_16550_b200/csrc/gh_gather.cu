@@ -25,10 +25,15 @@
 // which orders by value, then by the smallest bin.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gh_internal.cuh"
+#include "gh_ptx.cuh"
 
 namespace gh {
 namespace {
+
+using namespace ptx;
 
 // threads per CTA: 24 warps for power (K = 1) plans, 16 for the complex
 // K = 3 plans (more registers per thread)
@@ -45,7 +50,7 @@ struct GatherArgs {
   gh_grid grid;
   int64_t G;              // bins of the table (shard)
   int64_t bin0;           // global index of the shard's first bin
-  int64_t chunk_bins;     // full plan
+  int n_batches;          // trial batches (full plan: persistent work split)
   int full;
   int P, p4, M, T;
   float* map;             // parity mode [T][G]
@@ -57,13 +62,6 @@ __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDes
   if (a.full) return a.binid ? (int64_t)__ldg(a.binid + entry0 + lb) : a.bin0 + entry0 + lb;
   const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
-}
-
-// tie rule between two entries of one CTA: smaller global bin. Entry order is
-// bin order except in bank-permuted plans, where the bin ids decide.
-__device__ __forceinline__ bool entry_before(const GatherArgs& a, int64_t entry0, int x, int y) {
-  if (a.binid) return __ldg(a.binid + entry0 + x) < __ldg(a.binid + entry0 + y);
-  return x < y;
 }
 
 __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
@@ -121,42 +119,75 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   __shared__ float red_v[NW * TB];
   __shared__ int red_i[NW * TB];
 
-  // grid: x = location tile / bin chunk (fastest: every tile of a trial
-  // batch runs together, so the batch's spectra stay L2-resident), y = batch
-  const int tb = blockIdx.y;
-  const int64_t col = blockIdx.x;
+  const int P = PC ? PC : a.P;
+  __shared__ __align__(8) uint64_t stage_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&stage_bar, 1);
+    mbar_fence_init();
+  }
+  uint32_t phase = 0;
+
+  // Work items. Tiled plan: one (location tile = blockIdx.x, trial batch =
+  // blockIdx.y) per CTA; tiles of a batch run together, so the batch's
+  // spectra stay L2-resident. Full-ring plan: persistent CTAs; the
+  // (batch, 32-bin block) space is cut into gridDim.x equal contiguous runs,
+  // so every SM does the same work (no tail wave) and restages a ring only
+  // where its run enters a new batch.
+  int64_t u = 0, u_end = 1, nbpb = 1;
+  if (a.full) {
+    nbpb = (a.G + 31) / 32;
+    const int64_t U = nbpb * a.n_batches;
+    u = U * blockIdx.x / gridDim.x;
+    u_end = U * (blockIdx.x + 1) / gridDim.x;
+  }
+  while (u < u_end) {
+  int tb;
   int64_t entry0, nb;
   TileDesc td{};
   const int4* win;
   if (a.full) {
-    entry0 = col * a.chunk_bins;
-    nb = a.G - entry0 < a.chunk_bins ? a.G - entry0 : a.chunk_bins;
+    tb = static_cast<int>(u / nbpb);
+    const int64_t seg_end = (tb + 1) * nbpb < u_end ? (tb + 1) * nbpb : u_end;
+    entry0 = (u - tb * nbpb) * 32;
+    const int64_t e1 = (seg_end - tb * nbpb) * 32;
+    nb = (e1 < a.G ? e1 : a.G) - entry0;
     win = a.win;
+    u = seg_end;
   } else {
-    td = a.tiles[col];
+    tb = blockIdx.y;
+    td = a.tiles[blockIdx.x];
     entry0 = td.entry_off;
     nb = (int64_t)td.wx * td.wy * td.wz;
-    win = a.win + col * a.P;
+    win = a.win + blockIdx.x * a.P;
+    u = u_end;
   }
-  const int P = PC ? PC : a.P;
 
-  // ---- stage the windows: rows (base + r) mod M of every pair
+  // ---- stage the windows: rows (base + r) mod M of every pair. A window is
+  // a few contiguous row runs of the batch's spectra (split where it wraps
+  // the ring), so the TMA engine copies it with bulk copies while every
+  // thread waits on one mbarrier.
   const uint4* spec = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(a.spec) +
                                                      (int64_t)tb * a.P * a.M * TB * ES);
   uint4* sm4 = reinterpret_cast<uint4*>(smraw);
-  for (int p = 0; p < P; ++p) {
-    const int4 w = win[p];
-    const uint4* src = spec + (int64_t)p * a.M * L;
-    uint4* dst = sm4 + (int64_t)w.z * L;
-    const int n = w.y * L;
-    for (int c = threadIdx.x; c < n; c += kGatherThreads) {
-      const int r = c / L, q = c - r * L;
-      int gi = w.x + r;
-      while (gi >= a.M) gi -= a.M;
-      dst[c] = __ldg(src + (int64_t)gi * L + q);
+  __syncthreads();  // barrier initialised / previous item's readers done
+  if (threadIdx.x == 0) {
+    uint32_t total = 0;
+    for (int p = 0; p < P; ++p) total += (uint32_t)win[p].y * 16u * L;
+    mbar_expect_tx(&stage_bar, total);
+    for (int p = 0; p < P; ++p) {
+      const int4 w = win[p];
+      const uint4* src = spec + (int64_t)p * a.M * L;
+      uint4* dst = sm4 + (int64_t)w.z * L;
+      for (int r = 0, gi = w.x; r < w.y; gi = 0) {  // base in [0, M); K = 3 rings wrap twice
+        const int n = a.M - gi < w.y - r ? a.M - gi : w.y - r;
+        bulk_g2s(dst + (int64_t)r * L, src + (int64_t)gi * L, (uint32_t)n * 16u * L, &stage_bar);
+        r += n;
+      }
     }
+    mbar_arrive(&stage_bar);
   }
-  __syncthreads();
+  mbar_wait(&stage_bar, phase);
+  phase ^= 1u;
 
   // ---- gather
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -293,6 +324,7 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
       }
     }
   }
+  }  // work items
 }
 
 __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* idx, float* val) {
@@ -313,6 +345,15 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
+  if (a.full) {
+    // persistent: every resident CTA slot, but >= 4096 bins per CTA so the
+    // ring staging stays amortised
+    int occ = 0;
+    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gather_threads<K3>(), smem));
+    const int64_t work = a.n_batches * ((a.G + 31) / 32 * 32) / 4096;
+    grid = dim3(static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)std::max(occ, 1) * ctx->num_sms))));
+  }
   KTimer kt(ctx, "gather");
   kern<<<grid, gather_threads<K3>(), smem, ctx->stream>>>(a);
   GH_LAUNCHED(ctx);
@@ -366,19 +407,12 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.map = map_d;
   a.keys = keys_d;
   const int n_tb = (T + pl.tb - 1) / pl.tb;
-  int n_cols = pl.n_tiles;
-  if (pl.full) {
-    // split the bins so that ~2 waves of CTAs exist, but keep >= 4096 bins
-    // per CTA to amortise the staging of the whole ring
-    int64_t chunks = (2LL * ctx->num_sms + n_tb - 1) / n_tb;
-    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, (t->G + 4095) / 4096));
-    // multiple of 32: bank-complementary entry pairs stay on even offsets
-    a.chunk_bins = ((t->G + chunks - 1) / chunks + 31) / 32 * 32;
-    n_cols = static_cast<int>((t->G + a.chunk_bins - 1) / a.chunk_bins);
-  }
+  a.n_batches = n_tb;
   if (n_tb > 65535) fail(GH_EINVAL, "gather: too many trial batches for one launch");
   const size_t smem = static_cast<size_t>(pl.max_rows) * pl.tb * pl.esize;
-  dim3 grid(n_cols, n_tb);
+  // tiled plan: (tile, batch) CTAs; the full-ring plan's persistent grid is
+  // sized in run() from the occupancy
+  dim3 grid(pl.full ? 1 : pl.n_tiles, pl.full ? 1 : n_tb);
   const bool mag = combine == GH_MAGNITUDE;
   const bool mapmode = map_d != nullptr;
   if (!pl.k3) {

@@ -138,7 +138,6 @@ struct Plan {
   int esize = 4;          // staged element bytes (float power / float2 complex)
   int k3 = 0;             // 1: consecutive-triple combine with coefficients
   int p4 = 4;             // pairs padded to a multiple of 4 (row array stride)
-  int64_t chunk_bins = 0; // full plan: bins per CTA column
   int n_tiles = 0;
   int max_rows = 0;
   TileDesc* tiles_d = nullptr;   // tiled plan
