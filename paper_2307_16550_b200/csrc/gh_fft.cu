@@ -395,206 +395,325 @@ __global__ void __launch_bounds__(kFftThreads, 1) k_fft(FftArgs a) {
 }
 
 // ------------------------------------------------------------ fixed-size FFT
-// The same algorithm with N, os and the rows per pass as compile-time
-// constants (the BASELINE sizes): every shared-memory offset folds into an
-// immediate, which removes the index arithmetic that dominates the generic
-// kernel's instruction count.
+// The BASELINE sizes run a compile-time specialisation that works on two
+// rows (trials) at once with sm_100's packed fp32 instructions: a point of
+// a row pair is one float4 {re_a, re_b, im_a, im_b}, so every complex add is
+// two FADD2 and every twiddle product four FMUL2/FFMA2 (the twiddle is a
+// scalar-broadcast operand) for two trials — half the FP instructions and
+// half the shared-memory instructions of a per-row FFT. Each thread owns
+// exactly 16 points of every pass (one radix-16 task, or 16/R radix-R
+// tasks), so the passes run in place: load, DFT in registers, barrier,
+// store, barrier. All shared-memory offsets fold into immediates.
 __host__ __device__ constexpr int pad_c(int i) { return i + (i >> 4); }
 
-constexpr int kFxThreads = 256;
+struct Cx2 {  // one complex point of two rows: re = (a, b), im = (a, b)
+  float2 re, im;
+};
+__device__ __forceinline__ Cx2 cx_add(Cx2 a, Cx2 b) {
+  return {__fadd2_rn(a.re, b.re), __fadd2_rn(a.im, b.im)};
+}
+__device__ __forceinline__ Cx2 cx_sub(Cx2 a, Cx2 b) {
+  return {__fadd2_rn(a.re, make_float2(-b.re.x, -b.re.y)),
+          __fadd2_rn(a.im, make_float2(-b.im.x, -b.im.y))};
+}
+// x * (c + i s), c and s broadcast to both rows
+__device__ __forceinline__ Cx2 cx_mul(Cx2 x, float c, float s) {
+  return {__ffma2_rn(x.im, make_float2(-s, -s), __fmul2_rn(x.re, make_float2(c, c))),
+          __ffma2_rn(x.im, make_float2(c, c), __fmul2_rn(x.re, make_float2(s, s)))};
+}
+__device__ __forceinline__ Cx2 cx_mul_mi(Cx2 x) {  // x * -i
+  return {x.im, make_float2(-x.re.x, -x.re.y)};
+}
+__device__ __forceinline__ Cx2 cx_w16(Cx2 x, int e) {  // x * W16^e, e constant
+  e &= 15;
+  if (e == 0) return x;
+  if (e == 4) return cx_mul_mi(x);
+  if (e == 8) return {make_float2(-x.re.x, -x.re.y), make_float2(-x.im.x, -x.im.y)};
+  if (e == 12) return {make_float2(-x.im.x, -x.im.y), x.re};
+  return cx_mul(x, kC16[e], -kS16[e]);
+}
+__device__ __forceinline__ void cx_dft4(Cx2& a, Cx2& b, Cx2& c, Cx2& d) {
+  const Cx2 t0 = cx_add(a, c), t1 = cx_sub(a, c);
+  const Cx2 t2 = cx_add(b, d), t3 = cx_mul_mi(cx_sub(b, d));
+  a = cx_add(t0, t2);
+  c = cx_sub(t0, t2);
+  b = cx_add(t1, t3);
+  d = cx_sub(t1, t3);
+}
+// forward R-point DFT, natural order in and out (same factorisations as
+// dft_reg, constant indices only)
+template <int R>
+__device__ __forceinline__ void cx_dft(Cx2* v) {
+  if constexpr (R == 2) {
+    const Cx2 a = v[0], b = v[1];
+    v[0] = cx_add(a, b);
+    v[1] = cx_sub(a, b);
+  } else if constexpr (R == 4) {
+    cx_dft4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    Cx2 y[8];
+#pragma unroll
+    for (int n2 = 0; n2 < 2; ++n2) {
+      Cx2 a = v[n2], b = v[2 + n2], c = v[4 + n2], d = v[6 + n2];
+      cx_dft4(a, b, c, d);
+      y[0 * 2 + n2] = a;
+      y[1 * 2 + n2] = cx_w16(b, 2 * n2 * 1);
+      y[2 * 2 + n2] = cx_w16(c, 2 * n2 * 2);
+      y[3 * 2 + n2] = cx_w16(d, 2 * n2 * 3);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      const Cx2 a = y[k1 * 2], b = y[k1 * 2 + 1];
+      v[k1] = cx_add(a, b);
+      v[k1 + 4] = cx_sub(a, b);
+    }
+  } else {
+    static_assert(R == 16, "radix 2, 4, 8 or 16");
+    Cx2 y[16];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      Cx2 a = v[n2], b = v[4 + n2], c = v[8 + n2], d = v[12 + n2];
+      cx_dft4(a, b, c, d);
+      y[0 * 4 + n2] = a;
+      y[1 * 4 + n2] = cx_w16(b, n2 * 1);
+      y[2 * 4 + n2] = cx_w16(c, n2 * 2);
+      y[3 * 4 + n2] = cx_w16(d, n2 * 3);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      Cx2 a = y[k1 * 4 + 0], b = y[k1 * 4 + 1], c = y[k1 * 4 + 2], d = y[k1 * 4 + 3];
+      cx_dft4(a, b, c, d);
+      v[k1] = a;
+      v[k1 + 4] = b;
+      v[k1 + 8] = c;
+      v[k1 + 12] = d;
+    }
+  }
+}
+__device__ __forceinline__ Cx2 cx_ld(const float4* p) {
+  const float4 q = *p;
+  return {make_float2(q.x, q.y), make_float2(q.z, q.w)};
+}
+// two 8-byte stores: the DFT leaves re and im in unrelated register pairs,
+// and one 16-byte store would cost two register moves per point
+// (inline PTX: the compiler would merge the pair back into one STS.128)
+__device__ __forceinline__ void cx_st(float4* p, Cx2 v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.re.x), "f"(v.re.y) : "memory");
+  asm volatile("st.shared.v2.f32 [%0+8], {%1, %2};" ::"r"(a), "f"(v.im.x), "f"(v.im.y) : "memory");
+}
 
-template <int LN, int LOS, int LROWS>
+// LN = log2 N, LOS = log2 os, LP = log2 row pairs per group
+template <int LN, int LOS, int LP>
 struct Fx {
-  static constexpr int N = 1 << LN, OS = 1 << LOS, M = N * OS, ROWS = 1 << LROWS;
-  // padded sub-FFT stride, SUBP = 16/os (mod 16) float2: the os sub-rows
-  // holding consecutive output bins k = os*m + j land 32/os banks apart, so
-  // the epilogue's reads (consecutive k across lanes) are conflict-free
+  static constexpr int N = 1 << LN, OS = 1 << LOS, M = N * OS, PAIRS = 1 << LP, ROWS = 2 * PAIRS;
+  static constexpr int THREADS = PAIRS * M / 16;  // 16 points of every pass per thread
+  // padded sub-FFT stride in float4, SUBP = 8/os (mod 8): the os sub-rows
+  // holding consecutive output bins k = os*m + j land in distinct 16-byte
+  // bank groups, so the epilogue's reads (consecutive k across lanes) are
+  // conflict-free
   static constexpr int SUBP_BASE = N + N / 16;
-  static constexpr int SUBP_WANT = OS > 1 ? 16 / OS : 0;
-  static constexpr int SUBP = SUBP_BASE + ((SUBP_WANT - SUBP_BASE % 16) + 16) % 16;
-  static constexpr int PITCH = OS * SUBP + ((OS * SUBP) % 2 == 0 ? 1 : 0);
+  static constexpr int SUBP_WANT = OS > 1 ? 8 / OS : 0;
+  static constexpr int SUBP = SUBP_BASE + ((SUBP_WANT - SUBP_BASE % 8) + 8) % 8;
+  static constexpr int PITCH = OS * SUBP;  // float4 per row pair
   static constexpr int NP = (LN + 3) / 4;
   static constexpr int lr(int ps) { return LN - 4 * ps >= 4 ? 4 : LN - 4 * ps; }
-  static constexpr size_t smem_bytes() { return (2ull * ROWS * PITCH + N) * 8; }
-  static_assert(LN >= 4, "fixed FFT needs N >= 16");
+  static constexpr int TWN = N;             // pass twiddles (< N entries)
+  static constexpr int TWL = (OS - 1) * N;   // load twiddles W_M^{jn}, 1 <= j < os
+  static constexpr size_t smem_bytes() { return (size_t)PAIRS * PITCH * 16 + (TWN + TWL) * 8; }
+  static_assert(LN >= 4 && OS <= 8, "fixed FFT needs N >= 16, os <= 8");
+  static_assert(THREADS >= 32 && THREADS <= 1024, "fixed FFT block size");
 };
 
-template <int LN, int LOS, int LROWS, int PS>
-__device__ __forceinline__ void fixed_pass(const float2* __restrict__ src, float2* __restrict__ dst,
-                                           const float2* __restrict__ ptw) {
-  using F = Fx<LN, LOS, LROWS>;
+template <int LN, int LOS, int LP, int PS>
+__device__ __forceinline__ void fixed_pass(float4* __restrict__ buf, const float2* __restrict__ ptw) {
+  using F = Fx<LN, LOS, LP>;
   constexpr int LRR = F::lr(PS), R = 1 << LRR, NS = 1 << (4 * PS);
   constexpr int PER = F::N / R;
-  constexpr int TASKS = F::ROWS * F::OS * PER;
-  constexpr int TW0 = (1 << (4 * PS)) - 1;  // sum of previous radix-16 tables
+  constexpr int TPT = 16 / R;                // tasks per thread
+  constexpr int TW0 = (1 << (4 * PS)) - 1;   // sum of previous radix-16 tables
+  Cx2 v[TPT][R];
+  int sb[TPT], oo[TPT];
 #pragma unroll
-  for (int it = 0; it < (TASKS + kFxThreads - 1) / kFxThreads; ++it) {
-    const int task = threadIdx.x + it * kFxThreads;
-    if (TASKS % kFxThreads != 0 && task >= TASKS) break;
-    const int ro = task / PER, q = task % PER;
-    const int row = ro >> LOS, sub = ro & (F::OS - 1);
-    const int sbase = row * F::PITCH + sub * F::SUBP;
+  for (int it = 0; it < TPT; ++it) {
+    const int task = threadIdx.x + it * F::THREADS;
+    const int ro = task / PER, q = task % PER;  // ro = pair * os + sub
+    const int sbase = (ro >> LOS) * F::PITCH + (ro & (F::OS - 1)) * F::SUBP;
     const int k = q & (NS - 1);
-    float2 v[R];
-    if constexpr (PER % 16 == 0) {
-      const float2* s = src + sbase + pad_c(q);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = s[r * (PER + PER / 16)];
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = src[sbase + pad_c(q + r * PER)];
-    }
+    for (int r = 0; r < R; ++r) v[it][r] = cx_ld(buf + sbase + pad_c(q + r * PER));
     if constexpr (PS > 0) {
       const float2* t = ptw + TW0 + k * (R - 1);
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], t[r - 1]);
+      for (int r = 1; r < R; ++r) {
+        const float2 w = t[r - 1];
+        v[it][r] = cx_mul(v[it][r], w.x, w.y);
+      }
     }
-    dft_reg<R>(v);
-    const int o = (q - k) * R + k;
-    if constexpr (NS % 16 == 0) {
-      float2* d = dst + sbase + pad_c(o);
+    cx_dft<R>(v[it]);
+    sb[it] = sbase;
+    oo[it] = (q - k) * R + k;
+  }
+  __syncthreads();  // every point of the pass read: overwrite in place
 #pragma unroll
-      for (int r = 0; r < R; ++r) d[r * (NS + NS / 16)] = v[r];
-    } else {
-      // first pass: o = q * R is a multiple of 16 and r < 16
-      float2* d = dst + sbase + pad_c(o);
+  for (int it = 0; it < TPT; ++it) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) d[r] = v[r];
-    }
+    for (int r = 0; r < R; ++r) cx_st(buf + sb[it] + pad_c(oo[it] + r * NS), v[it][r]);
   }
   __syncthreads();
 }
 
-template <int LN, int LOS, int LROWS, int PS>
-__device__ __forceinline__ float2* fixed_passes(float2* src, float2* dst, const float2* ptw) {
-  using F = Fx<LN, LOS, LROWS>;
-  if constexpr (PS < F::NP) {
-    fixed_pass<LN, LOS, LROWS, PS>(src, dst, ptw);
-    return fixed_passes<LN, LOS, LROWS, PS + 1>(dst, src, ptw);
-  } else {
-    return src;
+template <int LN, int LOS, int LP, int PS>
+__device__ __forceinline__ void fixed_passes(float4* buf, const float2* ptw) {
+  if constexpr (PS < Fx<LN, LOS, LP>::NP) {
+    fixed_pass<LN, LOS, LP, PS>(buf, ptw);
+    fixed_passes<LN, LOS, LP, PS + 1>(buf, ptw);
   }
 }
 
-template <int LN, int LOS, int LROWS>
-__global__ void __launch_bounds__(kFxThreads) k_fft_fixed(FftArgs a) {
-  using F = Fx<LN, LOS, LROWS>;
-  constexpr int N = F::N, M = F::M, R = F::ROWS;
-  extern __shared__ float2 smem_dyn[];
-  __shared__ RowSynth rsm[16];
-  float2* ptw = smem_dyn;
-  float2* buf0 = smem_dyn + N;
-  float2* buf1 = buf0 + R * F::PITCH;
+// epilogue kinds of the fixed kernel (compile time)
+enum FxOut { FX_NATURAL = 0, FX_REAL = 1, FX_COMPLEX = 2 };
+
+template <int LN, int LOS, int LP, bool SYNTH, int KIND>
+__global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs a) {
+  using F = Fx<LN, LOS, LP>;
+  constexpr int N = F::N, M = F::M, PAIRS = F::PAIRS, ROWS = F::ROWS, NT = F::THREADS;
+  extern __shared__ float4 smem4[];
+  __shared__ RowSynth rsm[SYNTH ? ROWS : 1];
+  float4* buf = smem4;
+  float2* ptw = reinterpret_cast<float2*>(smem4 + PAIRS * F::PITCH);
+  float2* ltw = ptw + F::TWN;  // load twiddles W_M^{jn} at [(j-1) N + n]
   const int tb = blockIdx.x, p = blockIdx.y;
   const double inv_n = 1.0 / (double)N;
-  {
-    int toff = 0;
+  // pass twiddles: pass ps (stride NS, radix R) holds W_M^{r k M/(NS R)} at
+  // [k][r-1]; the first pass needs none
 #pragma unroll
-    for (int ps = 1; ps < F::NP; ++ps) {
-      const int lr = F::lr(ps), rp = 1 << lr, lns = 4 * ps, ns = 1 << lns;
-      toff = (1 << lns) - 1;
-      const int cnt = ns * (rp - 1);
-      const int step = LN + LOS - lns - lr;
-      for (int e = threadIdx.x; e < cnt; e += kFxThreads) {
-        const int k = e / (rp - 1), r = e - k * (rp - 1) + 1;
-        ptw[toff + e] = __ldg(a.tw + ((r * k) << step));
-      }
+  for (int ps = 1; ps < F::NP; ++ps) {
+    const int lr = F::lr(ps), rp = 1 << lr, lns = 4 * ps, ns = 1 << lns;
+    const int toff = (1 << lns) - 1;
+    const int cnt = ns * (rp - 1);
+    const int step = LN + LOS - lns - lr;
+    for (int e = threadIdx.x; e < cnt; e += NT) {
+      const int k = e / (rp - 1), r = e - k * (rp - 1) + 1;
+      ptw[toff + e] = __ldg(a.tw + ((r * k) << step));
     }
+  }
+  for (int e = threadIdx.x; e < (F::OS - 1) * N; e += NT) {
+    const int j = e / N + 1, n = e % N;
+    ltw[e] = __ldg(a.tw + j * n);
   }
   // frames of the next row group are fetched into registers while the
   // current group runs its passes (hides the HBM latency behind barriers)
-  constexpr int LPT = (R * N + kFxThreads - 1) / kFxThreads;
-  float2 pre[LPT];
+  constexpr int LPT = (PAIRS * N + NT - 1) / NT;
+  float2 pre[SYNTH ? 1 : LPT][2];
+  const float2* frames =  // row r of the batch at + r P N
+      SYNTH ? nullptr : a.frames + ((int64_t)tb * a.tb * a.P + p) * N;
+  const int rows_left = a.T - tb * a.tb;  // rows of this batch that exist
   auto fetch = [&](int g) {
 #pragma unroll
     for (int u = 0; u < LPT; ++u) {
-      const int e = threadIdx.x + u * kFxThreads;
-      float2 v = make_float2(0.f, 0.f);
-      if (e < R * N) {
-        const int t = tb * a.tb + g + (e >> LN);
-        if (t < a.T) v = __ldg(a.frames + ((int64_t)t * a.P + p) * N + (e & (N - 1)));
+      const int e = threadIdx.x + u * NT;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float2 v = make_float2(0.f, 0.f);
+        const int r = g + 2 * (e >> LN) + h;
+        if ((PAIRS * N % NT == 0 || e < PAIRS * N) && r < rows_left)
+          v = __ldg(frames + (int64_t)r * a.P * N + (e & (N - 1)));
+        pre[u][h] = v;
       }
-      pre[u] = v;
     }
   };
-  if (!a.synth) fetch(0);
-  for (int g0 = 0; g0 < a.tb; g0 += R) {
-    if (a.synth && threadIdx.x < R) {
-      const int t = tb * a.tb + g0 + threadIdx.x;
-      if (t < a.T) {
-        row_setup(a.sp, a.P, p, a.sp.trial0 + (uint64_t)t, rsm[threadIdx.x], a.sp.err_flag_d);
-        if (!a.sp.wrap)
-          for (int k = 0; k < a.sp.camp.n_targets; ++k) {
-            const double r = rsm[threadIdx.x].r[k];
-            if (!(r >= 0.0 && r < (double)N)) atomicOr(a.sp.err_flag_d, 1);
-          }
+  if constexpr (!SYNTH) fetch(0);
+  __syncthreads();  // twiddle tables
+  for (int g0 = 0; g0 < a.tb; g0 += ROWS) {
+    if constexpr (SYNTH) {
+      if (threadIdx.x < ROWS) {
+        const int t = tb * a.tb + g0 + threadIdx.x;
+        if (t < a.T) {
+          row_setup(a.sp, a.P, p, a.sp.trial0 + (uint64_t)t, rsm[threadIdx.x], a.sp.err_flag_d);
+          if (!a.sp.wrap)
+            for (int k = 0; k < a.sp.camp.n_targets; ++k) {
+              const double r = rsm[threadIdx.x].r[k];
+              if (!(r >= 0.0 && r < (double)N)) atomicOr(a.sp.err_flag_d, 1);
+            }
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
+    // load: sample n of the pair's rows -> sub-FFT j input y[n] W_M^{jn}
 #pragma unroll
     for (int u = 0; u < LPT; ++u) {
-      const int e = threadIdx.x + u * kFxThreads;
-      if (e >= R * N) break;
-      const int r = e >> LN;
+      const int e = threadIdx.x + u * NT;
+      if (PAIRS * N % NT != 0 && e >= PAIRS * N) break;
+      const int pp = e >> LN;
       const int n = e & (N - 1);
-      float2 v = pre[u];
-      if (a.synth) {
-        const int t = tb * a.tb + g0 + r;
-        v = t < a.T ? synth_sample(rsm[r], a.sp.camp.n_targets, n, inv_n) : make_float2(0.f, 0.f);
+      float2 ya, yb;
+      if constexpr (SYNTH) {
+        const int r = g0 + 2 * pp;
+        const float2 z = make_float2(0.f, 0.f);
+        ya = r < rows_left ? synth_sample(rsm[2 * pp], a.sp.camp.n_targets, n, inv_n) : z;
+        yb = r + 1 < rows_left ? synth_sample(rsm[2 * pp + 1], a.sp.camp.n_targets, n, inv_n) : z;
+      } else {
+        ya = pre[u][0];
+        yb = pre[u][1];
       }
-      float2* row = buf0 + r * F::PITCH + pad_c(n);
-      row[0] = v;
+      const Cx2 y{make_float2(ya.x, yb.x), make_float2(ya.y, yb.y)};
+      float4* row = buf + pp * F::PITCH + pad_c(n);
+      cx_st(row, y);
 #pragma unroll
-      for (int j = 1; j < F::OS; ++j) row[j * F::SUBP] = cmul(v, __ldg(a.tw + j * n));
+      for (int j = 1; j < F::OS; ++j) {
+        const float2 w = ltw[(j - 1) * N + n];
+        cx_st(row + j * F::SUBP, cx_mul(y, w.x, w.y));
+      }
     }
-    if (!a.synth && g0 + R < a.tb) fetch(g0 + R);
+    if constexpr (!SYNTH)
+      if (g0 + ROWS < a.tb) fetch(g0 + ROWS);
     __syncthreads();
-    const float2* sm = fixed_passes<LN, LOS, LROWS, 0>(buf0, buf1, ptw);
-    if (a.out_kind == FFT_NATURAL) {
+    fixed_passes<LN, LOS, LP, 0>(buf, ptw);
+    // epilogue: output bin k = os * m + j lives in sub-row j at m
+    if constexpr (KIND == FX_NATURAL) {
       float2* out = static_cast<float2*>(a.out);
-      for (int e = threadIdx.x; e < R * M; e += kFxThreads) {
-        const int r = e / M, k = e % M;
-        const int t = tb * a.tb + g0 + r;
+      for (int e = threadIdx.x; e < PAIRS * M; e += NT) {
+        const int pp = e / M, k = e % M;
+        const int t = tb * a.tb + g0 + 2 * pp;
         const int j = k & (F::OS - 1), m = k >> LOS;
-        if (t < a.T) out[((int64_t)t * a.P + p) * M + k] = sm[r * F::PITCH + j * F::SUBP + pad_c(m)];
+        const Cx2 z = cx_ld(buf + pp * F::PITCH + j * F::SUBP + pad_c(m));
+        if (t < a.T) out[((int64_t)t * a.P + p) * M + k] = make_float2(z.re.x, z.im.x);
+        if (t + 1 < a.T) out[((int64_t)(t + 1) * a.P + p) * M + k] = make_float2(z.re.y, z.im.y);
       }
     } else {
-      // one thread per range bin k: the R rows' values are contiguous in the
+      // one thread per range bin k: the group's rows are contiguous in the
       // gather layout [batch][pair][k][TB] -> vector stores
-      const int64_t base = ((int64_t)tb * a.P + p) * M;
+      const int64_t o0 = ((int64_t)tb * a.P + p) * M * a.tb + g0;
+      const bool mag = a.out_kind == FFT_GATHER_MAG;
 #pragma unroll 2
-      for (int k = threadIdx.x; k < M; k += kFxThreads) {
+      for (int k = threadIdx.x; k < M; k += NT) {
         const int j = k & (F::OS - 1), m = k >> LOS;
-        const float2* s = sm + j * F::SUBP + pad_c(m);
-        float2 z[R];
+        const float4* s = buf + j * F::SUBP + pad_c(m);
+        const int64_t o = o0 + (int64_t)k * a.tb;
+        if constexpr (KIND == FX_COMPLEX) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float2*>(a.out) + o);
 #pragma unroll
-        for (int r = 0; r < R; ++r) z[r] = s[r * F::PITCH];
-        const int64_t o = (base + k) * a.tb + g0;
-        if (a.out_kind == FFT_GATHER_COMPLEX) {
-          float2* dst = static_cast<float2*>(a.out) + o;
-          if constexpr (R % 2 == 0) {
-#pragma unroll
-            for (int r = 0; r < R; r += 2)
-              *reinterpret_cast<float4*>(dst + r) = make_float4(z[r].x, z[r].y, z[r + 1].x, z[r + 1].y);
-          } else {
-            dst[0] = z[0];
+          for (int pp = 0; pp < PAIRS; ++pp) {
+            const Cx2 z = cx_ld(s + pp * F::PITCH);
+            dst[pp] = make_float4(z.re.x, z.im.x, z.re.y, z.im.y);
           }
         } else {
-          float w[R];
+          float2 w[PAIRS];
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float pw = z[r].x * z[r].x + z[r].y * z[r].y;
-            w[r] = (a.out_kind == FFT_GATHER_MAG) ? sqrtf(pw) : pw;
+          for (int pp = 0; pp < PAIRS; ++pp) {
+            const Cx2 z = cx_ld(s + pp * F::PITCH);
+            w[pp] = __ffma2_rn(z.re, z.re, __fmul2_rn(z.im, z.im));
+            if (mag) w[pp] = make_float2(sqrtf(w[pp].x), sqrtf(w[pp].y));
           }
           float* dst = static_cast<float*>(a.out) + o;
-          if constexpr (R % 4 == 0) {
+          if constexpr (PAIRS % 2 == 0) {
 #pragma unroll
-            for (int r = 0; r < R; r += 4)
-              *reinterpret_cast<float4*>(dst + r) = make_float4(w[r], w[r + 1], w[r + 2], w[r + 3]);
-          } else if constexpr (R == 2) {
-            *reinterpret_cast<float2*>(dst) = make_float2(w[0], w[1]);
+            for (int pp = 0; pp < PAIRS; pp += 2)
+              *reinterpret_cast<float4*>(dst + 2 * pp) =
+                  make_float4(w[pp].x, w[pp].y, w[pp + 1].x, w[pp + 1].y);
           } else {
-            dst[0] = w[0];
+            *reinterpret_cast<float2*>(dst) = w[0];
           }
         }
       }
@@ -611,16 +730,31 @@ int ilog2(int v) {
 
 using FftKernel = void (*)(FftArgs);
 
-// compile-time instantiations: (log2 N, log2 os, log2 rows per pass); rows *
-// M = 4096 points per pass keeps a CTA near 70 KB (three CTAs per SM)
-FftKernel fixed_kernel(int ln, int los, int lrows, size_t* smem) {
-#define GH_FX(a, b, c)                              \
-  if (ln == a && los == b && lrows == c) {          \
-    *smem = Fx<a, b, c>::smem_bytes();              \
-    return k_fft_fixed<a, b, c>;                    \
+template <int LN, int LOS, int LP>
+FftKernel fixed_variant(bool synth, int out_kind, size_t* smem, int* threads) {
+  *smem = Fx<LN, LOS, LP>::smem_bytes();
+  *threads = Fx<LN, LOS, LP>::THREADS;
+  const int kind = out_kind == FFT_NATURAL ? FX_NATURAL
+                   : out_kind == FFT_GATHER_COMPLEX ? FX_COMPLEX : FX_REAL;
+  if (synth) {
+    if (kind == FX_NATURAL) return k_fft_fixed<LN, LOS, LP, true, FX_NATURAL>;
+    if (kind == FX_COMPLEX) return k_fft_fixed<LN, LOS, LP, true, FX_COMPLEX>;
+    return k_fft_fixed<LN, LOS, LP, true, FX_REAL>;
   }
-  GH_FX(6, 2, 4)   // N=64,   M=256  (small test scenes)
-  GH_FX(7, 0, 4)   // N=128,  M=128
+  if (kind == FX_NATURAL) return k_fft_fixed<LN, LOS, LP, false, FX_NATURAL>;
+  if (kind == FX_COMPLEX) return k_fft_fixed<LN, LOS, LP, false, FX_COMPLEX>;
+  return k_fft_fixed<LN, LOS, LP, false, FX_REAL>;
+}
+
+// compile-time instantiations: (log2 N, log2 os, log2 row pairs per group);
+// pairs * M = 4096 points (256 threads) where the trial batch allows
+FftKernel fixed_kernel(int ln, int los, int lp, bool synth, int out_kind, size_t* smem,
+                       int* threads) {
+#define GH_FX(a, b, c) \
+  if (ln == a && los == b && lp == c) return fixed_variant<a, b, c>(synth, out_kind, smem, threads);
+  GH_FX(6, 2, 2)   // N=64,   M=256  (small test scenes, 8-trial batches)
+  GH_FX(6, 2, 3)   // N=64,   M=256  (16-trial batches)
+  GH_FX(7, 0, 3)   // N=128,  M=128
   GH_FX(8, 2, 2)   // N=256,  M=1024 (c1, c2)
   GH_FX(9, 1, 2)   // N=512,  M=1024 (c4)
   GH_FX(9, 2, 1)   // N=512,  M=2048 (c5)
@@ -690,16 +824,21 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   a.out = out_d;
   size_t smem = bytes(R);
   int threads = kFftThreads;
-  // fixed-size kernel when this (N, os) has one: rows * M = 4096
-  int fr = 1;
-  while (fr * 2 <= (tb < 16 ? tb : 16) && fr * 2 * M <= 4096) fr *= 2;
+  // fixed-size row-pair kernel when this (N, os) has one: pairs * M <= 4096,
+  // at most 8 pairs, and the trial batch a whole number of row groups
+  int lp = -1;
+  if (tb >= 2) {
+    lp = ilog2(tb) - 1;
+    while (lp > 0 && ((M << lp) > 4096 || lp > 3)) --lp;
+  }
   size_t fsmem = 0;
-  FftKernel kern = fixed_kernel(a.log2n, a.log2os, ilog2(fr), &fsmem);
+  int fthreads = 0;
+  FftKernel kern = lp >= 0 ? fixed_kernel(a.log2n, a.log2os, lp, synth != nullptr, out_kind,
+                                          &fsmem, &fthreads)
+                           : nullptr;
   if (kern) {
-    a.rows = fr;
-    a.log2rows = ilog2(fr);
     smem = fsmem;
-    threads = kFxThreads;
+    threads = fthreads;
   } else {
     kern = k_fft;
   }
