@@ -1,6 +1,6 @@
 """Minimal driver for ncu: one config, a few hop steps (no bench extras).
 
-    python tools/prof_step.py [--config c2] [--steps 3] [--path frames|campaign|direct]
+    python tools/prof_step.py [--config c2] [--steps 3] [--path frames|topk|campaign|direct]
 """
 import argparse
 import sys
@@ -29,6 +29,8 @@ def main():
     for _ in range(a.steps):
         if a.path == "frames":
             gh.hop_argmax(ctx, table, frames)
+        elif a.path == "topk":
+            gh.hop_topk(ctx, table, frames, sc.topk)
         elif a.path == "campaign":
             gh.campaign_hop(ctx, table, sc, 0, T)
         else:
