@@ -171,12 +171,13 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
 }
 
 // Top-K local maxima per trial (BASELINE c3): maps of a trial chunk are
-// materialised (<= 1 GiB), then k_topk_localmax picks the peaks.
+// materialised (<= 8 GiB of the 180 GB HBM: ~2000 c3 trials, so the FFT and
+// gather launches fill the GPU), then k_topk_localmax picks the peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
   gh::build_plan(c, t);
   const int tb = t->plan.tb;
-  int64_t chunk = (int64_t(1) << 28) / std::max<int64_t>(t->G, 1);
+  int64_t chunk = (int64_t(1) << 31) / std::max<int64_t>(t->G, 1);
   chunk = std::max<int64_t>(tb, chunk / tb * tb);
   chunk = std::min<int64_t>(chunk, (T + tb - 1) / tb * tb);
   float* map = static_cast<float*>(c->mapbuf.get(sizeof(float) * chunk * t->G));

@@ -186,10 +186,8 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
     }
     mbar_arrive(&stage_bar);
   }
-  mbar_wait(&stage_bar, phase);
-  phase ^= 1u;
 
-  // ---- gather
+  // ---- gather (the first table block loads while the TMA staging lands)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / L, v = lane % L;
   const float4* smv = reinterpret_cast<const float4*>(smraw) + v;  // this lane's column
@@ -216,6 +214,8 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
     for (int q = 0; q < PQ; ++q)
       if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
   }
+  mbar_wait(&stage_bar, phase);
+  phase ^= 1u;
   for (int64_t blk = w0; blk < w1; blk += 32) {
     if (blk + 32 + lane < w1) {
 #pragma unroll
