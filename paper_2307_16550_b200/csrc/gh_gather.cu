@@ -35,9 +35,11 @@ namespace {
 
 using namespace ptx;
 
-// threads per CTA: 24 warps for power (K = 1) plans, 16 for the complex
-// K = 3 plans (more registers per thread)
-template <bool K3>
+// threads per CTA (one CTA per SM): 24 warps for power (K = 1) plans, 16
+// for the complex K = 3 plans (more registers per thread). Two CTAs per SM
+// with half-size windows were measured slower on c3/c4/c5: the windows'
+// staging bytes per bin grow faster than the overlap gains.
+template <bool K3, bool FULL>
 constexpr int gather_threads() { return K3 ? 512 : 768; }
 
 struct GatherArgs {
@@ -107,9 +109,9 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
 }
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
-__global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a) {
-  constexpr int kGatherThreads = gather_threads<K3>();
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL>
+__global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(GatherArgs a) {
+  constexpr int kGatherThreads = gather_threads<K3, FULL>();
   constexpr int ES = K3 ? 8 : 4;         // staged element bytes
   constexpr int L = TB * ES / 16;        // lanes per row (16 B each)
   constexpr int TPL = 16 / ES;           // trials per lane
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   // so every SM does the same work (no tail wave) and restages a ring only
   // where its run enters a new batch.
   int64_t u = 0, u_end = 1, nbpb = 1;
-  if (a.full) {
+  if constexpr (FULL) {
     nbpb = (a.G + 31) / 32;
     const int64_t U = nbpb * a.n_batches;
     u = U * blockIdx.x / gridDim.x;
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
   int64_t entry0, nb;
   TileDesc td{};
   const int4* win;
-  if (a.full) {
+  if constexpr (FULL) {
     tb = static_cast<int>(u / nbpb);
     const int64_t seg_end = (tb + 1) * nbpb < u_end ? (tb + 1) * nbpb : u_end;
     entry0 = (u - tb * nbpb) * 32;
@@ -198,7 +200,11 @@ __global__ void __launch_bounds__(gather_threads<K3>(), 1) k_gather(GatherArgs a
     best[i] = -1.0f;
     blb[i] = -1;
   }
-  const int64_t per_warp = ((nb + NW - 1) / NW + 31) / 32 * 32;
+  // full plans: 32-bin multiples (bank-complementary entry pairs stay on
+  // even offsets); tiled plans: warp-step multiples, so small tiles still
+  // spread over every warp
+  constexpr int64_t kRound = FULL ? 32 : BPW;
+  const int64_t per_warp = ((nb + NW - 1) / NW + kRound - 1) / kRound * kRound;
   const int64_t w0 = warp * per_warp;
   const int64_t w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);  // uint2 words (4 pairs) per bin
@@ -340,23 +346,35 @@ __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* id
   val[t] = __uint_as_float((unsigned)(k >> 32));
 }
 
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
-void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ>;
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL>
+void run_k(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
+  constexpr int NT = gather_threads<K3, FULL>();
+  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ, FULL>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
-  if (a.full) {
+  if (FULL) {
     // persistent: every resident CTA slot, but >= 4096 bins per CTA so the
     // ring staging stays amortised
     int occ = 0;
-    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, gather_threads<K3>(), smem));
+    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
     const int64_t work = a.n_batches * ((a.G + 31) / 32 * 32) / 4096;
     grid = dim3(static_cast<unsigned>(
         std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)std::max(occ, 1) * ctx->num_sms))));
   }
   KTimer kt(ctx, "gather");
-  kern<<<grid, gather_threads<K3>(), smem, ctx->stream>>>(a);
+  kern<<<grid, NT, smem, ctx->stream>>>(a);
   GH_LAUNCHED(ctx);
+}
+
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
+void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
+  if constexpr (TB == 16) {
+    if (a.full) {  // full-ring plans are built with 16-trial batches only
+      run_k<TB, K3, MAG, MAPMODE, PC, PQ, true>(ctx, a, grid, smem);
+      return;
+    }
+  }
+  run_k<TB, K3, MAG, MAPMODE, PC, PQ, false>(ctx, a, grid, smem);
 }
 
 // compile-time pair counts of the BASELINE configs (3, 16, 64), runtime

@@ -353,7 +353,8 @@ __global__ void k_fill_plan(FillArgs a) {
   }
 }
 
-constexpr size_t kStageBudget = 216 * 1024;
+constexpr size_t kStageBudget = 216 * 1024;  // full-ring plan: one CTA per SM
+constexpr size_t kTileBudget = 216 * 1024;   // tiled plans: one CTA per SM
 
 // Bank-conflict-aware bin order for the 16-trial full-ring power plan. A row
 // there is 64 bytes (half a shared-memory wavefront) and the gather serves
@@ -554,9 +555,9 @@ void build_plan(Ctx* ctx, Table* t) {
     // when there are many pairs (BASELINE c5: 64)
     pl.tb = pl.k3 ? 16 : 32;
     while (pl.tb > 8 &&
-           static_cast<int>(kStageBudget / (static_cast<size_t>(pl.tb) * pl.esize)) / P < 40)
+           static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize)) / P < 40)
       pl.tb >>= 1;
-    const int budget_rows = static_cast<int>(kStageBudget / (static_cast<size_t>(pl.tb) * pl.esize));
+    const int budget_rows = static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize));
     const int allow = budget_rows / P - 5;
     if (allow < 4) fail(GH_EINVAL, "gather plan: too many pairs for one shared-memory window");
     const gh_grid& g = t->grid;
