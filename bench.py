@@ -47,6 +47,36 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "fallback": True}
 
 
+# gather instantiation per BASELINE config: its ncu --set full capture in
+# profiles/ supplies roofline.traffic (DRAM read + write per launch)
+GATHER_KERNEL = {"c1": "k_gather<16, 0, 0, 0, 3, 1", "c2": "k_gather<16, 0, 0, 0, 3, 1",
+                 "c3": "k_gather<32, 0, 0, 0, 16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
+
+
+def ncu_traffic(config: str, trials: int):
+    """DRAM bytes per launch of the config's gather kernel from the newest
+    committed ncu --set full summary (profiles/r*_kernels_ncu_full.json),
+    scaled to `trials` (captures run tools/prof_step.py at their own trial
+    count, recorded in profiles/README.md); None when absent."""
+    want = GATHER_KERNEL.get(config)
+    files = sorted((ROOT / "profiles").glob("r*_kernels_ncu_full.json"))
+    if not want or not files:
+        return None
+    data = json.loads(files[-1].read_text())
+    for rep, kernels in data.items():
+        for k in kernels:
+            if want in k.get("kernel", "") and k.get("dram_read_bytes") is not None:
+                t0 = PROFILE_TRIALS.get(rep)
+                if not t0:
+                    continue
+                return (k["dram_read_bytes"] + k.get("dram_write_bytes", 0.0)) * trials / t0
+    return None
+
+
+# trials per launch of each committed capture (tools/evidence.sh)
+PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3g.ncu-rep": 4096}
+
+
 class ClockSampler:
     """SM clock + clock-event (throttle) reasons sampled through NVML every
     ~1 ms during the timed region (the same counters nvidia-smi reads; the
@@ -134,7 +164,7 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(sc, oi, oc, target_s: float = 12.0, kind: str = "port") -> dict:
+def cpu_baseline(sc, oi, oc, target_s: float = 30.0, kind: str = "port") -> dict:
     """The oracle's per-trial pipeline (synth -> FFT -> hop scan in 1024-bin
     chunks -> argmax) with parallel_for over trials on all host cores."""
     from oracle import oracle as O
@@ -342,9 +372,15 @@ def run_ours(args, world, rank, local):
     g_avg = g_ms / args.steps  # per step (top-K steps run the gather once per trial chunk)
     # shared-memory bytes gathered per unit: fp32 power (K = 1) or three
     # complex64 spectrum values (K = 3)
-    lsu_bytes = T * G * P * (4.0 if sc.k == 1 else 24.0)
-    achieved = lsu_bytes / (g_avg * 1e-3) / 1e9
-    hbm_bytes = T * P * sc.n_fft * 4.0 + G * 4 * 2  # staged spectra + table rows
+    # per launch (top-K steps launch the gather once per trial chunk)
+    g_launches = max(1, g_n // args.steps)
+    t_launch = T // g_launches
+    g_launch_ms = g_avg / g_launches
+    lsu_bytes = t_launch * G * P * (4.0 if sc.k == 1 else 24.0)
+    achieved = lsu_bytes / (g_launch_ms * 1e-3) / 1e9
+    # staged spectra (fp32 power, or complex64 for K = 3) + table rows
+    hbm_bytes = (t_launch * P * sc.n_fft * (4.0 if sc.k == 1 else 8.0) + G * 8
+                 + (G * P * 24 if sc.k == 3 else 0))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -363,13 +399,18 @@ def run_ours(args, world, rank, local):
                        **({"topk": k_ms / args.steps} if topk else {})},
         "launches_per_step": {"fft": f_n // args.steps, "gather": g_n // args.steps},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                     "frac": achieved / smem_peak, "traffic": None,
+                     "frac": achieved / smem_peak,
+                     "traffic": ncu_traffic(sc.name, t_launch),
+                     "launch_ms": g_launch_ms, "trials_per_launch": t_launch,
+                     "traffic_note": "DRAM read+write bytes per launch from the committed ncu "
+                                     "--set full capture (profiles/), compare with hbm."
+                                     "bytes_per_launch",
                      "kernel": (f"k_gather (map mode; top-{topk} local maxima by k_topk_localmax)"
                                 if topk else "k_gather (fused argmax)"),
                      "peak_source": "measured in-run (gh_measure_smem_peak, LDS.128 all SMs)",
                      "algorithmic_bytes_per_launch": lsu_bytes,
                      "hbm": {"bytes_per_launch": hbm_bytes,
-                             "achieved_gbs": hbm_bytes / (g_avg * 1e-3) / 1e9,
+                             "achieved_gbs": hbm_bytes / (g_launch_ms * 1e-3) / 1e9,
                              "peak_gbs": pk.get("hbm_gbs")}},
         "e2e": {"value": units_step / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": T * P * N * 16, "d2h_bytes_per_step": T * (8 + 4),
