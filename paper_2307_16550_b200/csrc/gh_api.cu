@@ -248,6 +248,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->twiddle_buf.release();
     c->aprep.release();
     c->mapbuf.release();
+    c->seeds.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)

@@ -58,6 +58,7 @@ struct UmmaArgs {
   float* map;
   unsigned long long* keys;
   const unsigned char* aprep;  // v2: prepared A stage blocks (k_prep_a)
+  const float2* seeds;         // v2: [P][N/8][G] exp(j 2 pi rho n) at n = 8 c (k_seeds)
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -349,6 +350,33 @@ __global__ void k_prep_a(const float2* __restrict__ frames, int T, int P, int N,
   }
 }
 
+// Steering phasor seeds, once per call: for every (pair, bin) the fp64
+// phase rho n (rho = r/N turns per sample) at n = 0, 8, 16, ... reduced and
+// evaluated with fp64 sincospi. The producers then only run the 8-sample
+// fp32 recurrence from a seed (no per-stage fp64 phase or sincospif).
+__global__ void k_seeds(const double* __restrict__ txrx, gh_grid grid, double scale, int P, int N,
+                        int64_t G, float2* __restrict__ seeds) {
+  const int n8 = N / 8;
+  const double inv_n = 1.0 / (double)N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)P * G;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(e / G);
+    const int64_t g = e - (int64_t)p * G;
+    double x[3];
+    dgrid_point(grid, g, x);
+    const double* tp = txrx + 6 * p;
+    const double r =
+        __dmul_rn(scale, __dadd_rn(dnorm3(tp, x[0], x[1], x[2]), dnorm3(tp + 3, x[0], x[1], x[2])));
+    const double rho = r * inv_n;
+    for (int c = 0; c < n8; ++c) {
+      const double ph = rho * (double)(8 * c);
+      double sn, cs;
+      sincospi(2.0 * (ph - floor(ph)), &sn, &cs);
+      seeds[((int64_t)p * n8 + c) * G + g] = make_float2((float)cs, (float)sn);
+    }
+  }
+}
+
 __device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
                                             float4 v) {
   uint4 b, s;
@@ -364,7 +392,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint64_t full[STAGES], empty[STAGES], acc_full, acc_empty;
   __shared__ uint32_t tmem_base_s;
-  __shared__ double rho_s[BG];    // r / N of the current pair (producers)
   __shared__ float2 wst_s[BG];    // exp(j 2 pi rho): one-sample phasor step
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -416,10 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
                                              dnorm3(tp + 3, x[0], x[1], x[2])));
           }
           const double rho = r * inv_n;
-          rho_s[pt] = rho;
-          float sw, cw;
-          sincospif((float)(2.0 * (rho - floor(rho))), &sw, &cw);
-          wst_s[pt] = make_float2(cw, sw);
+          double sw, cw;
+          sincospi(2.0 * (rho - floor(rho)), &sw, &cw);
+          wst_s[pt] = make_float2((float)cw, (float)sw);
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
@@ -442,9 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
       // B: bin `row`, samples nb + 8*half .. +7 (4 chunks), re and im rows
       {
         const int n_first = nb + 8 * half;
-        const double ph0 = rho_s[row] * (double)n_first;
-        float sn, cn;
-        sincospif((float)(2.0 * (ph0 - floor(ph0))), &sn, &cn);
+        const int64_t g = g0 + row;
+        const float2 sd = g < a.G ? __ldg(a.seeds + ((int64_t)p * (a.N / 8) + (n_first >> 3)) * a.G + g)
+                                  : make_float2(0.f, 0.f);
+        float sn = sd.y, cn = sd.x;
         const float2 w = wst_s[row];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -504,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
         __syncwarp();
       }
       // epilogue of pair p
-      mbar_wait(&acc_full, (uint32_t)p & 1u);
+      mbar_wait_sleep(&acc_full, (uint32_t)p & 1u, 256);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t row_addr = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll
@@ -582,6 +609,15 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
     const int KC = (2 * a.N) / BK;
     const size_t aprep_bytes = (size_t)tt * a.P * KC * (2 * TILE_BYTES_A);
     a.aprep = static_cast<const unsigned char*>(ctx->aprep.get(aprep_bytes));
+    {
+      KTimer kt(ctx, "direct_seeds");
+      float2* seeds = static_cast<float2*>(ctx->seeds.get(sizeof(float2) * a.P * (a.N / 8) * a.G));
+      const int64_t n = (int64_t)a.P * a.G;
+      const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
+      v2::k_seeds<<<blocks, 256, 0, ctx->stream>>>(txrx_d, *g, a.scale, a.P, a.N, a.G, seeds);
+      GH_LAUNCHED(ctx);
+      a.seeds = seeds;
+    }
     {
       KTimer kt(ctx, "direct_prep");
       const int64_t n16 = (int64_t)tt * BT * a.P * (a.N / 2);

@@ -61,7 +61,7 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds;
   int twiddle_m = 0;
   int direct_impl = 0;  // 0: tcgen05 3xTF32, 1: CUDA-core fp32 (reference path)
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
