@@ -139,6 +139,44 @@ int gh_table_info(const gh_table* t, int64_t* n_bins, int32_t* n_pairs,
 int gh_table_download(gh_table* t, uint32_t* idx, double* coef);
 int gh_table_destroy(gh_table* t);
 
+/* ---- GHT1 hop-table container ------------------------------------------
+ * save_hop_table / load_hop_table (src/interp.cpp:225-389, format
+ * include/gridhop/interp.hpp:69-77): little-endian magic "GHT1", u32
+ * version (1) / Q / bins / K / os / Ms, u64 scene hash, f64 worst residual,
+ * then per bin per pair K u32 indices and K (re, im) f64 pairs. Errors are
+ * GH_ERUNTIME with the reference's messages ("<path>: bad magic (not a GHT1
+ * hop table)", "<path>: truncated ...", "<path>: stale hop table (scene or
+ * grid mismatch)", ...). */
+typedef struct gh_ght1_header {
+  int32_t n_pairs;   /* Q: receivers of the reference, TX-RX pairs here */
+  int32_t n_bins;
+  int32_t k;         /* interpolation order 1..3 (polar tables store 3) */
+  int32_t os_range;
+  int32_t n_samples;
+  uint64_t scene_hash;
+  double max_residual;
+} gh_ght1_header;
+
+/* scene_hash (src/model.cpp:135-166): the reference's FNV-1a over the
+ * receiver count, chirps, samples, f0, bandwidth, chirp duration, the TX
+ * and every RX position (2-D, x then y). tx_xy[2], rx_xy[2 * n_rx]. */
+uint64_t gh_scene_hash(int32_t n_rx, int32_t n_chirps, int32_t n_samples, double f0,
+                       double bandwidth, double chirp_duration, const double* tx_xy,
+                       const double* rx_xy);
+/* Host arrays in the reference layout: idx u32 [bins][Q][K], coef f64
+ * [bins][Q][K][2]. gh_ght1_read with idx = coef = NULL reads and validates
+ * only the header; otherwise `capacity` (entries) must hold bins*Q*K. */
+int gh_ght1_write(const char* path, const gh_ght1_header* hdr, const uint32_t* idx,
+                  const double* coef);
+int gh_ght1_read(const char* path, gh_ght1_header* hdr, uint32_t* idx, double* coef,
+                 int64_t capacity);
+/* Device tables: save downloads the operator; load validates the file
+ * against the scene it is about to serve (hash, pairs, samples, os, bins:
+ * "stale hop table") and uploads it. */
+int gh_table_save(gh_table* t, const char* path, uint64_t scene_hash);
+int gh_table_load(gh_ctx* ctx, const char* path, const gh_wave* wave, const gh_grid* grid,
+                  uint64_t scene_hash, gh_table** out);
+
 /* ---- stage kernels (device pointers) ---------------------------------- */
 /* synthesize_frame + add_noise (src/synth.cpp:15-49) for trials
  * [trial0, trial0+T): frames complex64 [T][P][N]; truth fp64 [T][K][3]

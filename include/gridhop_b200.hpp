@@ -120,6 +120,30 @@ inline HopTable upload_hop_table(Context& ctx, const Scene& s, InterpScheme sche
   return HopTable(t);
 }
 
+// scene_hash (model.hpp / model.cpp:135-166) of a single-TX 2-D scene: the
+// key GHT1 files are bound to. rx_xy = {x0, y0, x1, y1, ...}.
+inline uint64_t scene_hash(int n_chirps, int n_samples, double f0, double bandwidth,
+                           double chirp_duration, const double tx_xy[2],
+                           const std::vector<double>& rx_xy) {
+  return gh_scene_hash(static_cast<int32_t>(rx_xy.size() / 2), n_chirps, n_samples, f0, bandwidth,
+                       chirp_duration, tx_xy, rx_xy.data());
+}
+
+// save_hop_table (interp.hpp:72): the device operator as a GHT1 file
+inline void save_hop_table(const std::string& path, const HopTable& table, uint64_t scene_hash) {
+  check(gh_table_save(table.get(), path.c_str(), scene_hash));
+}
+
+// load_hop_table (interp.hpp:76-77): refuses files built for another scene
+// or grid ("stale hop table"), then uploads
+inline HopTable load_hop_table(Context& ctx, const std::string& path, const Scene& s,
+                               uint64_t scene_hash) {
+  const gh_wave w = s.wave();
+  gh_table* t = nullptr;
+  check(gh_table_load(ctx.get(), path.c_str(), &w, &s.grid, scene_hash, &t));
+  return HopTable(t);
+}
+
 struct Estimates {
   std::vector<int64_t> bin;  // per trial, argmax_index rule (direct.cpp:55-62)
   std::vector<double> value;

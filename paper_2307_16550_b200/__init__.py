@@ -12,12 +12,14 @@ from .api import (Context, HopTable, InvalidArgument, GridhopRuntimeError, Domai
                   synthesize, fast_time_spectra,
                   hop_decision_map, hop_argmax, hop_estimate, campaign_hop, hop_topk,
                   campaign_hop_topk, topk_local_max,
-                  location_decision_map, direct_argmax, argmax_index, lib, exported_symbols)
+                  location_decision_map, direct_argmax, argmax_index, lib, exported_symbols,
+                  scene_hash, ght1_write, ght1_read, table_save, table_load)
 
 __all__ = [
     "scene", "Scene", "baseline", "small", "Context", "HopTable", "InvalidArgument",
     "GridhopRuntimeError", "DomainError", "CudaError", "precompute_hop_table",
     "upload_hop_table", "synthesize", "fast_time_spectra", "hop_decision_map", "hop_argmax",
     "hop_estimate", "campaign_hop", "location_decision_map", "direct_argmax", "argmax_index",
-    "lib", "exported_symbols",
+    "lib", "exported_symbols", "precompute_hop_table_shard", "hop_topk", "campaign_hop_topk",
+    "topk_local_max", "scene_hash", "ght1_write", "ght1_read", "table_save", "table_load",
 ]

@@ -44,6 +44,13 @@ class CudaError(RuntimeError):
 
 _EXC = {1: InvalidArgument, 2: GridhopRuntimeError, 3: DomainError, 4: CudaError}
 
+
+class Ght1Header(C.Structure):
+    """gh_ght1_header: the GHT1 container header (interp.hpp:69-71)."""
+    _fields_ = [("n_pairs", C.c_int32), ("n_bins", C.c_int32), ("k", C.c_int32),
+                ("os_range", C.c_int32), ("n_samples", C.c_int32), ("scene_hash", C.c_uint64),
+                ("max_residual", C.c_double)]
+
 _lib = None
 
 
@@ -92,6 +99,11 @@ def lib() -> C.CDLL:
             "gh_topk_local_max_d": (C.c_int, [vp, P(CGrid), vp, i32, i32, vp, vp]),
             "gh_direct_map_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp]),
             "gh_direct_argmax_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp, vp]),
+            "gh_scene_hash": (u64, [i32, i32, i32, f64, f64, f64, vp, vp]),
+            "gh_ght1_write": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp]),
+            "gh_ght1_read": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp, i64]),
+            "gh_table_save": (C.c_int, [vp, C.c_char_p, u64]),
+            "gh_table_load": (C.c_int, [vp, C.c_char_p, P(CWave), P(CGrid), u64, P(vp)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -259,6 +271,53 @@ def upload_hop_table(ctx: Context, scene: Scene, scheme: int, idx: np.ndarray,
     w, g = scene.c_wave(), scene.c_grid()
     _check(lib().gh_table_upload(ctx.h, C.byref(w), C.byref(g), scheme, idx.ctypes.data, cptr,
                                  C.byref(h)))
+    return HopTable(ctx, scene, h)
+
+
+def scene_hash(n_chirps: int, n_samples: int, f0: float, bandwidth: float,
+               chirp_duration: float, tx_xy, rx_xy) -> int:
+    """scene_hash (src/model.cpp:135-166) of a single-TX 2-D geometry."""
+    tx = np.ascontiguousarray(tx_xy, dtype=np.float64).reshape(2)
+    rx = np.ascontiguousarray(rx_xy, dtype=np.float64).reshape(-1, 2)
+    return int(lib().gh_scene_hash(rx.shape[0], n_chirps, n_samples, f0, bandwidth, chirp_duration,
+                                   tx.ctypes.data, rx.ctypes.data))
+
+
+def ght1_write(path: str, idx: np.ndarray, coef: np.ndarray, os_range: int, n_samples: int,
+               scene_hash: int, max_residual: float = 0.0) -> None:
+    """save_hop_table (src/interp.cpp:293-317) of a host table [G][P][K]."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    coef = np.ascontiguousarray(coef, dtype=np.complex128)
+    G, P, K = idx.shape
+    h = Ght1Header(P, G, K, os_range, n_samples, scene_hash, max_residual)
+    _check(lib().gh_ght1_write(str(path).encode(), C.byref(h), idx.ctypes.data, coef.ctypes.data))
+
+
+def ght1_read(path: str):
+    """load_hop_table's parser (src/interp.cpp:319-380): (header dict, idx
+    uint32 [G,P,K], coeffs complex128 [G,P,K])."""
+    h = Ght1Header()
+    _check(lib().gh_ght1_read(str(path).encode(), C.byref(h), None, None, 0))
+    shape = (h.n_bins, h.n_pairs, h.k)
+    n = h.n_bins * h.n_pairs * h.k
+    idx = np.empty(n, dtype=np.uint32)
+    coef = np.empty(n, dtype=np.complex128)
+    _check(lib().gh_ght1_read(str(path).encode(), C.byref(h), idx.ctypes.data, coef.ctypes.data, n))
+    hdr = {f: getattr(h, f) for f, _ in Ght1Header._fields_}
+    return hdr, idx.reshape(shape), coef.reshape(shape)
+
+
+def table_save(table: HopTable, path: str, scene_hash: int) -> None:
+    """save_hop_table of a device table (GHT1)."""
+    _check(lib().gh_table_save(table.h, str(path).encode(), scene_hash))
+
+
+def table_load(ctx: Context, path: str, scene: Scene, scene_hash: int) -> HopTable:
+    """load_hop_table: validated against `scene` ("stale hop table"), uploaded."""
+    h = C.c_void_p()
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_table_load(ctx.h, str(path).encode(), C.byref(w), C.byref(g), scene_hash,
+                               C.byref(h)))
     return HopTable(ctx, scene, h)
 
 

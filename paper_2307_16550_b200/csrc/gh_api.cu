@@ -8,6 +8,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <fstream>
+#include <iterator>
 #include <new>
 #include <string>
 #include <vector>
@@ -208,6 +211,138 @@ __global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
     out[i] = make_float2((float)v.x, (float)v.y);
   }
 }
+
+
+// ------------------------------------------------------------ GHT1 container
+// Restates save_hop_table / load_hop_table (src/interp.cpp:225-389): the same
+// little-endian byte layout and the same runtime_error texts.
+constexpr uint32_t kGht1Version = 1;
+
+struct Ght1Reader {
+  const char* p;
+  size_t left;
+  const std::string& path;
+  void need(size_t n, const char* what) const {
+    if (left < n)
+      fail(GH_ERUNTIME, path + ": truncated " + what + " (need " + std::to_string(n) +
+                            " bytes, have " + std::to_string(left) + ")");
+  }
+  template <class T>
+  T get(const char* what) {
+    need(sizeof(T), what);
+    T v;
+    std::memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    left -= sizeof(T);
+    return v;
+  }
+};
+
+template <class T>
+void ght1_put(std::string& out, T v) {
+  out.append(reinterpret_cast<const char*>(&v), sizeof v);
+}
+
+std::string ght1_read_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(GH_ERUNTIME, path + ": cannot open");
+  std::string data((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  if (in.bad()) fail(GH_ERUNTIME, path + ": read failed");
+  return data;
+}
+
+void ght1_write(const std::string& path, const gh_ght1_header& h, const uint32_t* idx,
+                const double* coef) {
+  if (h.n_pairs < 1 || h.n_bins < 1 || h.k < 1 || h.k > 3 || h.os_range < 1 || h.n_samples < 1)
+    fail(GH_EINVAL, "hop table: invalid GHT1 header");
+  const size_t entries = (size_t)h.n_bins * (size_t)h.n_pairs * (size_t)h.k;
+  std::string out;
+  out.reserve(44 + entries * 20);
+  out.append("GHT1", 4);
+  ght1_put<uint32_t>(out, kGht1Version);
+  ght1_put<uint32_t>(out, (uint32_t)h.n_pairs);
+  ght1_put<uint32_t>(out, (uint32_t)h.n_bins);
+  ght1_put<uint32_t>(out, (uint32_t)h.k);
+  ght1_put<uint32_t>(out, (uint32_t)h.os_range);
+  ght1_put<uint32_t>(out, (uint32_t)h.n_samples);
+  ght1_put<uint64_t>(out, h.scene_hash);
+  ght1_put<double>(out, h.max_residual);
+  // [bin][pair]: K indices, then K (re, im) — the reference's entry order
+  for (size_t e = 0; e < entries; e += (size_t)h.k) {
+    for (int j = 0; j < h.k; ++j) ght1_put<uint32_t>(out, idx[e + j]);
+    for (int j = 0; j < h.k; ++j) {
+      ght1_put<double>(out, coef ? coef[2 * (e + j)] : 1.0);
+      ght1_put<double>(out, coef ? coef[2 * (e + j) + 1] : 0.0);
+    }
+  }
+  std::ofstream f(path, std::ios::binary | std::ios::trunc);
+  if (!f) fail(GH_ERUNTIME, path + ": cannot open for writing");
+  f.write(out.data(), static_cast<std::streamsize>(out.size()));
+  f.flush();
+  if (!f) fail(GH_ERUNTIME, path + ": short write");
+}
+
+// header (+ payload when idx/coef are given: capacity entries)
+void ght1_read(const std::string& path, gh_ght1_header& h, uint32_t* idx, double* coef,
+               int64_t capacity) {
+  const std::string data = ght1_read_file(path);
+  Ght1Reader rd{data.data(), data.size(), path};
+  rd.need(4, "magic");
+  if (std::memcmp(rd.p, "GHT1", 4) != 0)
+    fail(GH_ERUNTIME, path + ": bad magic (not a GHT1 hop table)");
+  rd.p += 4;
+  rd.left -= 4;
+  const uint32_t version = rd.get<uint32_t>("version");
+  if (version != kGht1Version)
+    fail(GH_ERUNTIME, path + ": unsupported hop table version " + std::to_string(version));
+  h.n_pairs = (int32_t)rd.get<uint32_t>("receiver count");
+  h.n_bins = (int32_t)rd.get<uint32_t>("bin count");
+  h.k = (int32_t)rd.get<uint32_t>("order");
+  h.os_range = (int32_t)rd.get<uint32_t>("oversampling");
+  h.n_samples = (int32_t)rd.get<uint32_t>("sample count");
+  h.scene_hash = rd.get<uint64_t>("scene hash");
+  h.max_residual = rd.get<double>("worst residual");
+  if (h.k < 1 || h.k > 3)
+    fail(GH_ERUNTIME, path + ": unsupported interpolation order " + std::to_string(h.k));
+  const size_t entries = (size_t)(uint32_t)h.n_bins * (size_t)(uint32_t)h.n_pairs * (size_t)h.k;
+  const size_t payload = entries * (4 + 16);
+  if (rd.left < payload)
+    fail(GH_ERUNTIME, path + ": truncated (expected " + std::to_string(payload) +
+                          " payload bytes, have " + std::to_string(rd.left) + ")");
+  if (rd.left > payload)
+    fail(GH_ERUNTIME, path + ": payload size mismatch (expected " + std::to_string(payload) +
+                          " bytes, have " + std::to_string(rd.left) + ")");
+  if (!idx && !coef) return;
+  if (!idx || !coef || capacity < (int64_t)entries)
+    fail(GH_EINVAL, "hop table: GHT1 output arrays too small");
+  const uint32_t n_fft = (uint32_t)h.n_samples * (uint32_t)h.os_range;
+  for (size_t e = 0; e < entries; e += (size_t)h.k) {
+    for (int j = 0; j < h.k; ++j) {
+      const uint32_t v = rd.get<uint32_t>("index");
+      if (v >= n_fft)
+        fail(GH_ERUNTIME, path + ": index " + std::to_string(v) + " outside the FFT grid");
+      idx[e + j] = v;
+    }
+    for (int j = 0; j < h.k; ++j) {
+      coef[2 * (e + j)] = rd.get<double>("coefficient");
+      coef[2 * (e + j) + 1] = rd.get<double>("coefficient");
+    }
+  }
+}
+
+// scene_hash (src/model.cpp:135-166), including the reference's offset basis
+struct Fnv1a {
+  uint64_t h = 1469598103934665603ull;
+  void feed(const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      h ^= b[i];
+      h *= 1099511628211ull;
+    }
+  }
+  void u32(uint32_t v) { feed(&v, sizeof v); }
+  void f64(double v) { feed(&v, sizeof v); }
+};
 
 }  // namespace
 
@@ -726,6 +861,91 @@ int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
     gh::launch_decode_keys(c, keys, n_trials, idx_d, val_d);
     GH_CUDA(cudaStreamSynchronize(c->stream));
     txrx.release();
+  });
+}
+
+uint64_t gh_scene_hash(int32_t n_rx, int32_t n_chirps, int32_t n_samples, double f0,
+                       double bandwidth, double chirp_duration, const double* tx_xy,
+                       const double* rx_xy) {
+  Fnv1a f;
+  f.u32(static_cast<uint32_t>(n_rx));
+  f.u32(static_cast<uint32_t>(n_chirps));
+  f.u32(static_cast<uint32_t>(n_samples));
+  f.f64(f0);
+  f.f64(bandwidth);
+  f.f64(chirp_duration);
+  f.f64(tx_xy ? tx_xy[0] : 0.0);
+  f.f64(tx_xy ? tx_xy[1] : 0.0);
+  for (int q = 0; q < n_rx && rx_xy; ++q) {
+    f.f64(rx_xy[2 * q]);
+    f.f64(rx_xy[2 * q + 1]);
+  }
+  return f.h;
+}
+
+int gh_ght1_write(const char* path, const gh_ght1_header* hdr, const uint32_t* idx,
+                  const double* coef) {
+  return guarded([&] {
+    if (!path || !hdr || !idx) fail(GH_EINVAL, "hop table: null argument");
+    ght1_write(path, *hdr, idx, coef);
+  });
+}
+
+int gh_ght1_read(const char* path, gh_ght1_header* hdr, uint32_t* idx, double* coef,
+                 int64_t capacity) {
+  return guarded([&] {
+    if (!path || !hdr) fail(GH_EINVAL, "hop table: null argument");
+    ght1_read(path, *hdr, idx, coef, capacity);
+  });
+}
+
+int gh_table_save(gh_table* table, const char* path, uint64_t scene_hash) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!t || !path) fail(GH_EINVAL, "hop table: null argument");
+    if (t->bin0 != 0 || t->G != (int64_t)t->grid.n[0] * t->grid.n[1] * t->grid.n[2])
+      fail(GH_EINVAL, "hop table: a grid shard cannot be saved as GHT1");
+    if (t->G > 0xffffffffll) fail(GH_EINVAL, "hop table: too many bins for GHT1");
+    const int64_t n = t->G * t->P * t->K;
+    std::vector<uint32_t> idx(static_cast<size_t>(n));
+    std::vector<double> coef(static_cast<size_t>(2 * n));
+    const int st = gh_table_download(table, idx.data(), coef.data());
+    if (st != GH_OK) fail(st, g_err);
+    gh_ght1_header h{};
+    h.n_pairs = t->P;
+    h.n_bins = static_cast<int32_t>(t->G);
+    h.k = t->K;
+    h.os_range = t->os;
+    h.n_samples = t->N;
+    h.scene_hash = scene_hash;
+    h.max_residual = t->max_residual;
+    ght1_write(path, h, idx.data(), coef.data());
+  });
+}
+
+int gh_table_load(gh_ctx* ctx, const char* path, const gh_wave* wave, const gh_grid* grid,
+                  uint64_t scene_hash, gh_table** out) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !path || !out) fail(GH_EINVAL, "hop table: null argument");
+    check_wave(wave);
+    const int64_t G = grid_size(grid);
+    gh_ght1_header h{};
+    ght1_read(path, h, nullptr, nullptr, 0);
+    // bind to the scene and grid this table is about to serve
+    // (interp.cpp:382-386; os_range too, since the spectra follow the wave)
+    if (h.scene_hash != scene_hash || h.n_pairs != wave->n_pairs ||
+        h.n_samples != wave->n_samples || h.os_range != wave->os_range || (int64_t)h.n_bins != G)
+      fail(GH_ERUNTIME, std::string(path) + ": stale hop table (scene or grid mismatch)");
+    const int64_t n = G * h.n_pairs * h.k;
+    std::vector<uint32_t> idx(static_cast<size_t>(n));
+    std::vector<double> coef(static_cast<size_t>(2 * n));
+    ght1_read(path, h, idx.data(), coef.data(), n);
+    gh_table* t = nullptr;
+    const int st = gh_table_upload(ctx, wave, grid, h.k, idx.data(), coef.data(), &t);
+    if (st != GH_OK) fail(st, g_err);
+    reinterpret_cast<gh::Table*>(t)->max_residual = h.max_residual;
+    *out = t;
   });
 }
 

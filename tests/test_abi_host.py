@@ -62,6 +62,53 @@ def test_cpp_wrapper_header_compiles(tmp_path):
     assert r.returncode == 0, r.stderr
 
 
+def test_cpp_program_links_and_runs_the_host_abi(tmp_path):
+    """A reference-side C++ caller: compiles against the wrappers, links the
+    library and runs its host-only entry points (scene hash, GHT1 container,
+    reference error texts) without a GPU."""
+    src = tmp_path / "ght1.cpp"
+    src.write_text(r'''
+#include "gridhop_b200.hpp"
+#include <cstdio>
+#include <cstring>
+int main(int argc, char** argv) {
+  namespace gb = gridhop::b200;
+  const double tx[2] = {0.0, 0.0};
+  const uint64_t h = gb::scene_hash(16, 64, 77e9, 250e6, 20e-6, tx, {10, 0, 0, 10, -10, 0.5});
+  gh_ght1_header hd{3, 2, 2, 4, 64, h, 0.25};
+  uint32_t idx[12] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11};
+  double coef[24];
+  for (int i = 0; i < 24; ++i) coef[i] = 0.5 * i;
+  gb::check(gh_ght1_write(argv[1], &hd, idx, coef));
+  gh_ght1_header back{};
+  uint32_t idx2[12];
+  double coef2[24];
+  gb::check(gh_ght1_read(argv[1], &back, idx2, coef2, 12));
+  if (back.scene_hash != h || std::memcmp(idx, idx2, sizeof idx) ||
+      std::memcmp(coef, coef2, sizeof coef))
+    return 2;
+  try {
+    gb::check(gh_ght1_read("/nonexistent.ght", &back, nullptr, nullptr, 0));
+  } catch (const std::runtime_error& e) {
+    std::printf("%llu|%s\n", (unsigned long long)h, e.what());
+    return 0;
+  }
+  return 3;
+}
+''')
+    exe = tmp_path / "ght1"
+    lib_dir = ROOT / "paper_2307_16550_b200"
+    r = subprocess.run(["g++", "-std=c++17", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
+                        f"-L{lib_dir}", "-lgridhop_b200", f"-Wl,-rpath,{lib_dir}"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe), str(tmp_path / "t.ght")], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    h, msg = r.stdout.strip().split("|")
+    assert int(h) == gh.scene_hash(16, 64, 77e9, 250e6, 20e-6, [0, 0], [[10, 0], [0, 10], [-10, 0.5]])
+    assert msg == "/nonexistent.ght: cannot open"
+
+
 def test_host_rng_matches_oracle():
     from oracle import oracle as O
     for seed, a, b in ((0, 0, 0), (20260816, 5, 0x53434E), (2**63 + 7, 99999, 3)):
