@@ -101,9 +101,12 @@ __device__ __forceinline__ float2 synth_sample(const RowSynth& rs, int K, int n,
     y.y += a.x * s + a.y * c;
   }
   if (rs.sigma != 0.0) {
+    // the counter-based draws are the oracle's bit for bit; the Rayleigh
+    // transform runs in fp32 (1 - u1 formed exactly in fp64, >= 2^-53, so
+    // the log stays finite): ~1e-7 relative, inside the 2e-5 frame tolerance
     const double u1 = uniform01(rs.noise_key, 2ull * n);
     const double u2 = uniform01(rs.noise_key, 2ull * n + 1);
-    const float amp = (float)(rs.sigma * sqrt(-log1p(-u1)));
+    const float amp = (float)rs.sigma * sqrtf(-logf((float)(1.0 - u1)));
     float s, c;
     sincospif((float)(2.0 * u2), &s, &c);
     y.x += amp * c;
