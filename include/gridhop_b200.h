@@ -102,10 +102,11 @@ int gh_ctx_launch_count(gh_ctx* ctx, int64_t* count);
 int gh_ctx_set_timing(gh_ctx* ctx, int32_t on);
 int gh_ctx_kernel_time(gh_ctx* ctx, const char* name, double* total_ms, int64_t* count);
 int gh_ctx_reset_timing(gh_ctx* ctx);
-/* Direct-method engine: 0 = tcgen05 tensor cores, 3xTF32, warp-specialised
- * pipeline (default); 1 = CUDA-core fp32 contraction (the reference path the
- * tensor-core kernels are checked and timed against); 2 = single-stage
- * tcgen05 kernel (v1). */
+/* Direct-method engine: 0 = tcgen05 tensor cores, 3xFP16 (kind::f16 on
+ * power-of-two-scaled frames), warp-specialised pipeline (default); 1 =
+ * CUDA-core fp32 contraction (the reference path the tensor-core kernels are
+ * checked and timed against); 2 = single-stage tcgen05 3xTF32 kernel (v1);
+ * 3 = the warp-specialised pipeline in 3xTF32 (kind::tf32). */
 int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
 /* Diagnostics: measured shared-memory (LSU) read bandwidth of the device,
  * GB/s, all SMs — the roofline denominator of the gather kernel. */

@@ -185,9 +185,11 @@ class Context:
         _check(lib().gh_ctx_reset_timing(self.h))
 
     def set_direct_impl(self, impl: str) -> None:
-        """'tcgen05' (default: warp-specialised 3xTF32 tensor-core pipeline),
-        'tcgen05_v1' (single-stage tensor-core kernel) or 'simt' (CUDA-core fp32)."""
-        _check(lib().gh_ctx_set_direct_impl(self.h, {"tcgen05": 0, "simt": 1, "tcgen05_v1": 2}[impl]))
+        """'tcgen05' (default: warp-specialised 3xFP16 tensor-core pipeline),
+        'tcgen05_tf32' (the same pipeline in 3xTF32), 'tcgen05_v1' (single-stage
+        3xTF32 kernel) or 'simt' (CUDA-core fp32)."""
+        _check(lib().gh_ctx_set_direct_impl(
+            self.h, {"tcgen05": 0, "simt": 1, "tcgen05_v1": 2, "tcgen05_tf32": 3}[impl]))
 
     def smem_peak_gbps(self) -> float:
         v = C.c_double()

@@ -384,6 +384,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->aprep.release();
     c->mapbuf.release();
     c->seeds.release();
+    c->amax.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)
@@ -440,8 +441,10 @@ int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     if (!c) fail(GH_EINVAL, "ctx: null argument");
-    if (impl < 0 || impl > 2)
-      fail(GH_EINVAL, "ctx: direct impl must be 0 (tcgen05), 1 (simt) or 2 (tcgen05 v1)");
+    if (impl < 0 || impl > 3)
+      fail(GH_EINVAL,
+           "ctx: direct impl must be 0 (tcgen05 3xFP16), 1 (simt), 2 (tcgen05 v1) or 3 (tcgen05 "
+           "3xTF32)");
     c->direct_impl = impl;
   });
 }

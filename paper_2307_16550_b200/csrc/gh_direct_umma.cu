@@ -23,7 +23,10 @@
 // Operand layout (canonical K-major, no swizzle): core matrices of 8 rows x
 // 16 bytes, stored [k-chunk of 16 B][row group of 8][row][16 B], so
 // SBO = 128 B (row groups) and LBO = rows/8 * 128 B (k-chunks).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+#include <string>
 
 #include "gh_internal.cuh"
 #include "gh_ptx.cuh"
@@ -59,6 +62,7 @@ struct UmmaArgs {
   unsigned long long* keys;
   const unsigned char* aprep;  // v2: prepared A stage blocks (k_prep_a)
   const float2* seeds;         // v2: [P][N/8][G] exp(j 2 pi rho n) at n = 8 c (k_seeds)
+  const unsigned* amax;        // v2 fp16: bits of max |frame component| (k_absmax)
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -312,41 +316,109 @@ constexpr int B_BYTES = NC * BK * 4;   // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
 constexpr int LBOA = BT / 8 * 128;
 constexpr int LBOB = NC / 8 * 128;
+// instruction descriptors: fp32 accumulate, K-major A and B, M = BT, N = NC;
+// operands tf32 (format 2, kind::tf32) or fp16 (format 0, kind::f16)
 constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NC >> 3) << 17) |
                              ((uint32_t)(BT >> 4) << 24);
+constexpr uint32_t kIdescH = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(NC >> 3) << 17) |
+                             ((uint32_t)(BT >> 4) << 24);
 
+// one 32-byte K step: K = 8 tf32 or K = 16 fp16 elements
+template <bool H>
 __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdesc2), "r"(acc));
+  if constexpr (H) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdescH), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc2), "r"(acc));
+  }
+}
+
+// fp16 3-term split (3xFP16): hi = fp16(x), lo = fp16(x - hi); 8 values per
+// 16-byte chunk
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void split_store8(unsigned char* big, unsigned char* sml, int off,
+                                             const float (&v)[8]) {
+  float hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    hi[i] = __half2float(__float2half_rn(v[i]));
+    lo[i] = v[i] - hi[i];
+  }
+  *reinterpret_cast<uint4*>(big + off) =
+      make_uint4(pack_h2(hi[0], hi[1]), pack_h2(hi[2], hi[3]), pack_h2(hi[4], hi[5]),
+                 pack_h2(hi[6], hi[7]));
+  *reinterpret_cast<uint4*>(sml + off) =
+      make_uint4(pack_h2(lo[0], lo[1]), pack_h2(lo[2], lo[3]), pack_h2(lo[4], lo[5]),
+                 pack_h2(lo[6], lo[7]));
+}
+
+// power-of-two scale that brings the largest frame component into [1, 2)
+// (fp16 range and lo-part precision); exact to undo
+__device__ __forceinline__ int amax_exp(const unsigned* amax) {
+  const float m = __uint_as_float(*amax);
+  return m > 0.f ? ilogbf(m) : 0;
+}
+
+__global__ void k_absmax(const float* __restrict__ x, int64_t n, unsigned* out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // >= 0: order-preserving
 }
 
 __device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
                                             float4 v);
 
-// A operand prepared once per call: frames split into tf32 big/small and
-// laid out exactly as one stage's smem tile (canonical K-major), so a stage
-// is one contiguous 32 KB block: [trial tile][pair][k chunk][big | small].
+// A operand prepared once per call: frames split into big/small (tf32, or
+// fp16 after the power-of-two scale) and laid out exactly as one stage's smem
+// tile (canonical K-major), so a stage is one contiguous 32 KB block:
+// [trial tile][pair][k chunk][big | small].
+template <bool H>
 __global__ void k_prep_a(const float2* __restrict__ frames, int T, int P, int N,
-                         unsigned char* __restrict__ out) {
-  const int KC = (2 * N) / BK;
-  const int64_t n16 = (int64_t)((T + BT - 1) / BT) * BT * P * (N / 2);  // 16-byte chunks
+                         const unsigned* amax, unsigned char* __restrict__ out) {
+  constexpr int CPS = H ? 4 : 2;   // complex samples per 16-byte chunk
+  const int NCH = N / CPS;         // chunks along K per pair
+  const int KC = NCH / KCH;        // stages per pair
+  const float scale = H ? ldexpf(1.f, -amax_exp(amax)) : 1.f;
+  const int64_t n16 = (int64_t)((T + BT - 1) / BT) * BT * P * NCH;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n16;
        e += (int64_t)gridDim.x * blockDim.x) {
     // e -> (trial tile, pair, k chunk, 16-byte chunk in stage, row), row fastest
     const int row = (int)(e % BT);
     int64_t r = e / BT;
-    const int c16 = (int)(r % (N / 2));  // global 16-byte chunk along K (2 samples)
-    r /= (N / 2);
+    const int c16 = (int)(r % NCH);  // global 16-byte chunk along K
+    r /= NCH;
     const int p = (int)(r % P);
     const int tt = (int)(r / P);
     const int t = tt * BT + row;
     const int kc = c16 / KCH, kin = c16 % KCH;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < T) v = __ldg(reinterpret_cast<const float4*>(frames + ((int64_t)t * P + p) * N) + c16);
     unsigned char* blk = out + (((int64_t)tt * P + p) * KC + kc) * (2 * A_BYTES);
-    split_store(blk, blk + A_BYTES, kmaj_off(row, kin, LBOA), v);
+    const float4* src = reinterpret_cast<const float4*>(frames + ((int64_t)t * P + p) * N);
+    if constexpr (H) {
+      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+      if (t < T) {
+        v0 = __ldg(src + 2 * c16);
+        v1 = __ldg(src + 2 * c16 + 1);
+      }
+      const float v[8] = {v0.x * scale, v0.y * scale, v0.z * scale, v0.w * scale,
+                          v1.x * scale, v1.y * scale, v1.z * scale, v1.w * scale};
+      split_store8(blk, blk + A_BYTES, kmaj_off(row, kin, LBOA), v);
+    } else {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < T) v = __ldg(src + c16);
+      split_store(blk, blk + A_BYTES, kmaj_off(row, kin, LBOA), v);
+    }
   }
 }
 
@@ -388,7 +460,9 @@ __device__ __forceinline__ void split_store(unsigned char* big, unsigned char* s
   *reinterpret_cast<uint4*>(sml + off) = s;
 }
 
+template <bool H>
 __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
+  constexpr int SPS = H ? 32 : 16;  // complex samples per stage (128-byte rows)
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint64_t full[STAGES], empty[STAGES], acc_full, acc_empty;
   __shared__ uint32_t tmem_base_s;
@@ -397,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.y * BT;           // trial tile (slow) ...
   const int64_t g0 = (int64_t)blockIdx.x * BG;  // ... bin tile (fast): A stays in L2
-  const int KC = (2 * a.N) / BK;            // K chunks per pair
+  const int KC = a.N / SPS;                 // stages per pair
   const int n_stage = a.P * KC;
 
   if (warp == 0) {
@@ -455,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
       unsigned char* asml = base + A_BYTES;
       unsigned char* bbig = base + 2 * A_BYTES;
       unsigned char* bsml = bbig + B_BYTES;
-      const int nb = kc0 * (BK / 2);  // first complex sample of the chunk
+      const int nb = kc0 * SPS;  // first complex sample of the stage
       // A: the prepared big|small stage block, one TMA bulk copy; its bytes
       // complete on full[s] together with the producers' arrivals
       if (pt == 0) {
@@ -465,8 +539,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
         bulk_g2s(abig, src, 2 * A_BYTES, &full[s]);
       }
       (void)asml;
-      // B: bin `row`, samples nb + 8*half .. +7 (4 chunks), re and im rows
-      {
+      // B: bin `row`, samples nb + (SPS/2) half .. (4 chunks), re and im rows
+      if constexpr (H) {
+        // 16 samples, 4 per 16-byte chunk of 8 fp16; N % 32 == 0, so every
+        // sample of a stage is inside the frame
+        const int n_first = nb + 16 * half;
+        const int64_t g = g0 + row;
+        const float2 sd = g < a.G ? __ldg(a.seeds + ((int64_t)p * (a.N / 8) + (n_first >> 3)) * a.G + g)
+                                  : make_float2(0.f, 0.f);
+        float sn = sd.y, cn = sd.x;
+        const float2 w = wst_s[row];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float re[8], im[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            re[2 * u] = cn;
+            re[2 * u + 1] = sn;
+            im[2 * u] = -sn;
+            im[2 * u + 1] = cn;
+            const float c1 = cn * w.x - sn * w.y;
+            sn = cn * w.y + sn * w.x;
+            cn = c1;
+          }
+          const int kc = half * 4 + c;
+          split_store8(bbig, bsml, kmaj_off(row, kc, LBOB), re);
+          split_store8(bbig, bsml, kmaj_off(BG + row, kc, LBOB), im);
+        }
+      } else {
         const int n_first = nb + 8 * half;
         const int64_t g = g0 + row;
         const float2 sd = g < a.G ? __ldg(a.seeds + ((int64_t)p * (a.N / 8) + (n_first >> 3)) * a.G + g)
@@ -520,9 +620,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
               const uint64_t das = umma_desc(as_ + 2 * k * LBOA, LBOA, 128);
               const uint64_t dbb = umma_desc(bb + 2 * k * LBOB, LBOB, 128);
               const uint64_t dbs = umma_desc(bs + 2 * k * LBOB, LBOB, 128);
-              mma(tmem, dab, dbb, (kc0 > 0 || k > 0) ? 1u : 0u);
-              mma(tmem, dab, dbs, 1u);
-              mma(tmem, das, dbb, 1u);
+              mma<H>(tmem, dab, dbb, (kc0 > 0 || k > 0) ? 1u : 0u);
+              mma<H>(tmem, dab, dbs, 1u);
+              mma<H>(tmem, das, dbb, 1u);
             }
             mma_commit(&empty[s]);
           }
@@ -549,7 +649,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty);
     }
-    // final: map or per-trial argmax over this warp's 64 bins
+    // final: map or per-trial argmax over this warp's 64 bins (fp16: undo
+    // the frames' power-of-two scale, exactly)
+    if constexpr (H) {
+      const int e = amax_exp(a.amax);
+      const float unscale = ldexpf(1.f, a.mag ? e : 2 * e);
+#pragma unroll
+      for (int j = 0; j < 64; ++j) pw[j] *= unscale;
+    }
     const int t = t0 + q * 32 + lane;
     const int64_t gb0 = g0 + 64 * h;
     if (t < a.T) {
@@ -600,13 +707,17 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
   a.keys = keys_d;
   if (a.P > kMaxPairs) fail(GH_EINVAL, "direct: at most 64 TX-RX pairs");
   if (a.N % 2) fail(GH_EINVAL, "direct: n_samples must be even");
-  if (ctx->direct_impl == 0) {
-    if ((2 * a.N) % BK) fail(GH_EINVAL, "direct: n_samples must be a multiple of 16");
+  if (ctx->direct_impl == 0 || ctx->direct_impl == 3) {
+    // 0: 3xFP16 (kind::f16), 3: 3xTF32 (kind::tf32); both warp-specialised
+    const bool h16 = ctx->direct_impl == 0;
+    const int sps = h16 ? 32 : 16;
+    if (a.N % sps)
+      fail(GH_EINVAL, std::string("direct: n_samples must be a multiple of ") + std::to_string(sps));
     const int64_t gbt = (a.G + v2::BG - 1) / v2::BG;
     const int tt = (T + BT - 1) / BT;
     if (tt > 65535) fail(GH_EINVAL, "direct: too many trials for one launch");
     const size_t smem2 = v2::STAGES * v2::STAGE_BYTES;
-    const int KC = (2 * a.N) / BK;
+    const int KC = a.N / sps;
     const size_t aprep_bytes = (size_t)tt * a.P * KC * (2 * TILE_BYTES_A);
     a.aprep = static_cast<const unsigned char*>(ctx->aprep.get(aprep_bytes));
     {
@@ -620,17 +731,32 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
     }
     {
       KTimer kt(ctx, "direct_prep");
-      const int64_t n16 = (int64_t)tt * BT * a.P * (a.N / 2);
+      unsigned* amax = static_cast<unsigned*>(ctx->amax.get(sizeof(unsigned)));
+      a.amax = amax;
+      if (h16) {
+        GH_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), ctx->stream));
+        const int64_t nf = (int64_t)T * a.P * a.N * 2;
+        const int blocks = static_cast<int>(std::min<int64_t>((nf + 255) / 256, 148LL * 8));
+        v2::k_absmax<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const float*>(frames_d), nf,
+                                                      amax);
+        GH_LAUNCHED(ctx);
+      }
+      const int64_t n16 = (int64_t)tt * BT * a.P * (a.N / (h16 ? 4 : 2));
       const int blocks = static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 148LL * 32));
-      v2::k_prep_a<<<blocks, 256, 0, ctx->stream>>>(frames_d, T, a.P, a.N,
-                                                    const_cast<unsigned char*>(a.aprep));
+      if (h16)
+        v2::k_prep_a<true><<<blocks, 256, 0, ctx->stream>>>(frames_d, T, a.P, a.N, amax,
+                                                            const_cast<unsigned char*>(a.aprep));
+      else
+        v2::k_prep_a<false><<<blocks, 256, 0, ctx->stream>>>(frames_d, T, a.P, a.N, amax,
+                                                             const_cast<unsigned char*>(a.aprep));
       GH_LAUNCHED(ctx);
     }
-    GH_CUDA(cudaFuncSetAttribute(v2::k_direct_umma2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = h16 ? v2::k_direct_umma2<true> : v2::k_direct_umma2<false>;
+    GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem2)));
     dim3 grid2(static_cast<unsigned>(gbt), tt);
     KTimer kt(ctx, "direct_umma");
-    v2::k_direct_umma2<<<grid2, v2::kThreads, smem2, ctx->stream>>>(a);
+    kern<<<grid2, v2::kThreads, smem2, ctx->stream>>>(a);
     GH_LAUNCHED(ctx);
     return;
   }

@@ -61,9 +61,9 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax;
   int twiddle_m = 0;
-  int direct_impl = 0;  // 0: tcgen05 3xTF32, 1: CUDA-core fp32 (reference path)
+  int direct_impl = 0;  // 0: tcgen05 3xFP16, 1: CUDA-core fp32, 2: tcgen05 v1, 3: tcgen05 3xTF32
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
   cudaStream_t copy_stream = nullptr;
   bool ev_ready = false;

@@ -156,7 +156,7 @@ def test_campaign_matches_oracle_campaign(ctx):
     assert np.allclose(g_val.cpu().numpy(), o_val, rtol=1e-4)
 
 
-@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_v1", "simt"])
+@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_tf32", "tcgen05_v1", "simt"])
 @pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
 def test_direct_map_and_argmax(ctx, combine, impl):
     sc = S.small()
@@ -172,6 +172,21 @@ def test_direct_map_and_argmax(ctx, combine, impl):
         assert_argmax_parity(ref, idx.cpu().numpy(), f"direct {impl}")
     finally:
         ctx.set_direct_impl("tcgen05")
+
+
+@pytest.mark.parametrize("gain", [3.7e4, 2.5e-5])
+def test_direct_fp16_frame_scaling(ctx, gain):
+    # 3xFP16 scales frames by a power of two into [1, 2) before the fp16
+    # split (fp16 max 65504, subnormals below 6e-5) and undoes it exactly
+    sc = S.small()
+    fr, _ = O.synth(sc, 11, 9)
+    fr = fr * gain
+    ref = O.direct_map(sc, fr)
+    fd = frames_to_dev(fr)
+    m = gh.location_decision_map(ctx, sc, fd).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, _ = gh.direct_argmax(ctx, sc, fd)
+    assert_argmax_parity(ref, idx.cpu().numpy(), f"direct fp16 x{gain}")
 
 
 def test_direct_tcgen05_c2_scale(ctx):
