@@ -173,6 +173,11 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
       const int64_t g = g0 + (int64_t)u * kTopkThreads + threadIdx.x;
       const bool act = g < n4;
       const uint32_t i = (uint32_t)(h + 4 * g);
+      // float pre-filter: key > prune key implies value >= its value, so a
+      // float4 whose four values are all below it is skipped in one vote
+      const float tv = w.thr ? unord(static_cast<uint32_t>(w.thr >> 32)) : -INFINITY;
+      const bool any4 = act && (q[u].x >= tv || q[u].y >= tv || q[u].z >= tv || q[u].w >= tv);
+      if (!__any_sync(0xffffffffu, any4)) continue;
       warp_offer(w, wq, m, q[u].x, i, act, K, nx, ny, nz, &cta_thr);
       warp_offer(w, wq, m, q[u].y, i + 1, act, K, nx, ny, nz, &cta_thr);
       warp_offer(w, wq, m, q[u].z, i + 2, act, K, nx, ny, nz, &cta_thr);
