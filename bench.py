@@ -74,7 +74,8 @@ def ncu_traffic(config: str, trials: int):
 
 
 # trials per launch of each committed capture (tools/evidence.sh)
-PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3g.ncu-rep": 4096}
+PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3g.ncu-rep": 4096, "prof_tk2.ncu-rep": 512,
+                  "prof_direct_r1.ncu-rep": 1024}
 
 
 class ClockSampler:
