@@ -372,6 +372,31 @@ def run_ours(args, world, rank, local):
                   "hop_direct_argmax_agreement": agree,
                   "api": "gh_direct_argmax_d (tcgen05 kind::f16, 3xFP16)"}
 
+    # ---- indirect pipeline location stage (range peaks + multilateration,
+    # src/indirect.cpp:10-83): the reference's third comparison arm
+    indirect = None
+    if not args.no_direct and sc.name in ("c1", "c2"):
+        for _ in range(2):
+            gh.indirect_argmin(ctx, sc, frames)
+        ctx.synchronize()
+        ctx.reset_timing()
+        ctx.set_timing(True)
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            i0.record(stream)
+            for _ in range(args.direct_steps):
+                _, iidx, _ = gh.indirect_argmin(ctx, sc, frames)
+            i1.record(stream)
+        ctx.synchronize()
+        ctx.set_timing(False)
+        ims = i0.elapsed_time(i1) / args.direct_steps
+        ml_ms, ml_n = ctx.kernel_time("multilaterate")
+        indirect = {"ms_per_step": ims, "trials_per_s": T * world / (ims * 1e-3),
+                    "multilaterate_ms": ml_ms / max(ml_n, 1),
+                    "hop_indirect_argmax_agreement": float(np.mean(iidx.cpu().numpy()
+                                                                   == idx.cpu().numpy())),
+                    "api": "gh_indirect_argmin_d (FFT, range peaks, fp64 multilateration)"}
+
     if rank != 0:
         if dist:
             tdist.destroy_process_group()
@@ -431,6 +456,8 @@ def run_ours(args, world, rank, local):
     }
     if direct:
         line["direct"] = direct
+    if indirect:
+        line["indirect"] = indirect
     if world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
         oi, oc, _ = O.build_table(sc)

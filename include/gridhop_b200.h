@@ -140,6 +140,21 @@ int gh_table_info(const gh_table* t, int64_t* n_bins, int32_t* n_pairs,
 int gh_table_download(gh_table* t, uint32_t* idx, double* coef);
 int gh_table_destroy(gh_table* t);
 
+/* ---- indirect pipeline, location stage ---------------------------------
+ * range_doppler_map + RangeDopplerMap::peak + multilaterate_location
+ * (src/indirect.cpp:10-83) at Mc = 1: per (trial, pair) r_hat = (first
+ * maximum bin of the zero-padded range spectrum modulus) / os_range, then the
+ * grid bin minimising sum_q (sensed_range(x) - r_hat_q)^2 (first minimum),
+ * evaluated in fp64 exactly as the reference. frames complex64 [T][P][N];
+ * rhat_d fp64 [T][P] (output, nullable); idx int64 [T]; res fp64 [T]. */
+int gh_indirect_argmin_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                         const float* frames_d, int32_t n_trials, double* rhat_d,
+                         int64_t* idx_d, double* res_d);
+/* multilaterate_location alone, from caller range estimates rhat_d [T][P]. */
+int gh_multilaterate_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                       const double* rhat_d, int32_t n_trials, int64_t* idx_d,
+                       double* res_d);
+
 /* ---- GHT1 hop-table container ------------------------------------------
  * save_hop_table / load_hop_table (src/interp.cpp:225-389, format
  * include/gridhop/interp.hpp:69-77): little-endian magic "GHT1", u32

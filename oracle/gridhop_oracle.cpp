@@ -770,6 +770,70 @@ int or_direct_map(const double* frames, int32_t n_trials, const or_wave* w,
   });
 }
 
+// Indirect pipeline, location stage (src/indirect.cpp:10-83) at Mc = 1:
+// range_doppler_map of one receiver's frame is the modulus of its
+// zero-padded range spectrum (n_d = os_doppler * 1 rows; os_doppler = 1), its
+// peak() the first maximum in row-major order, r_hat = col / os_range
+// (indirect.cpp:27-29, 41-56). spectra [rows][m][2] (or_spectra's layout).
+int or_range_peaks(const double* spectra, int64_t rows, int32_t m, int32_t os_range,
+                   double* rhat) {
+  return guarded([&] {
+    if (os_range < 1) throw std::invalid_argument("range_doppler_map: oversampling must be >= 1");
+    for (int64_t r = 0; r < rows; ++r) {
+      const double* z = spectra + 2 * static_cast<size_t>(m) * r;
+      double best = -1.0;
+      int32_t col = 0;
+      for (int32_t k = 0; k < m; ++k) {
+        const double v = std::sqrt(z[2 * k] * z[2 * k] + z[2 * k + 1] * z[2 * k + 1]);
+        if (v > best) {
+          best = v;
+          col = k;
+        }
+      }
+      rhat[r] = static_cast<double>(col) / static_cast<double>(os_range);
+    }
+  });
+}
+
+// multilaterate_location (indirect.cpp:58-83): argmin over the grid of
+// sum_q (sensed_range(x) - r_hat_q)^2, q ascending, first minimum wins.
+// rhat [T][P]; idx [T]; residual [T].
+int or_multilaterate(const or_wave* w, const or_grid* g, const double* rhat, int32_t n_trials,
+                     int n_threads, int64_t* idx, double* residual) {
+  return guarded([&] {
+    check_wave(*w);
+    const int64_t G = grid_size(*g);
+    if (G <= 0) throw std::invalid_argument("multilateration: empty grid");
+    const int P = w->n_pairs;
+    std::vector<double> r(static_cast<size_t>(G) * P);
+    for (int64_t b = 0; b < G; ++b) {
+      double x[3];
+      grid_point(*g, b, x);
+      for (int p = 0; p < P; ++p)
+        r[static_cast<size_t>(b) * P + p] =
+            sensed_range(w->range_scale, w->tx + 3 * p, w->rx + 3 * p, x);
+    }
+    parallel_for(n_trials, n_threads, [&](int64_t t) {
+      const double* rh = rhat + static_cast<size_t>(t) * P;
+      double best = -1.0;
+      int64_t bi = 0;
+      for (int64_t b = 0; b < G; ++b) {
+        double res = 0.0;
+        for (int p = 0; p < P; ++p) {
+          const double d = r[static_cast<size_t>(b) * P + p] - rh[p];
+          res += d * d;
+        }
+        if (best < 0.0 || res < best) {
+          best = res;
+          bi = b;
+        }
+      }
+      idx[t] = bi;
+      residual[t] = best;
+    });
+  });
+}
+
 int64_t or_argmax(const double* v, int64_t n) {
   int64_t r = -1;
   if (guarded([&] { r = argmax(v, n); }) != 0) return -1;

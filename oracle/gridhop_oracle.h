@@ -100,6 +100,11 @@ int or_hop_map(const double* spectra, int32_t n_trials, int32_t n_pairs,
 int or_direct_map(const double* frames, int32_t n_trials, const or_wave* w,
                   const or_grid* g, int magnitude, int n_threads, double* map);
 int64_t or_argmax(const double* v, int64_t n);
+/* Indirect pipeline, location stage (src/indirect.cpp:10-83, Mc = 1). */
+int or_range_peaks(const double* spectra, int64_t rows, int32_t m, int32_t os_range,
+                   double* rhat);
+int or_multilaterate(const or_wave* w, const or_grid* g, const double* rhat, int32_t n_trials,
+                     int n_threads, int64_t* idx, double* residual);
 int or_topk_local_max(const double* map, const or_grid* g, int32_t k,
                       int64_t* idx_out, double* val_out);
 

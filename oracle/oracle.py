@@ -57,6 +57,8 @@ def lib():
             "or_direct_map": (C.c_int, [vp, i32, P(CWave), P(CGrid), C.c_int, C.c_int, vp]),
             "or_argmax": (i64, [vp, i64]),
             "or_topk_local_max": (C.c_int, [vp, P(CGrid), i32, vp, vp]),
+            "or_range_peaks": (C.c_int, [vp, i64, i32, i32, vp]),
+            "or_multilaterate": (C.c_int, [P(CWave), P(CGrid), vp, i32, C.c_int, vp, vp]),
             "or_campaign_hop": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), vp, vp, i32, C.c_int,
                                           C.c_int, u64, i32, C.c_int, vp, vp]),
             "or_campaign_direct": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), C.c_int, C.c_int,
@@ -169,6 +171,28 @@ def argmax(v: np.ndarray) -> int:
     if r < 0:
         raise OracleError(1, lib().or_last_error().decode())
     return int(r)
+
+
+def range_peaks(spec: np.ndarray, os_range: int) -> np.ndarray:
+    """r_hat per row of complex spectra [..., M]: range_doppler_map +
+    RangeDopplerMap::peak at Mc = 1 (src/indirect.cpp:10-56)."""
+    spec = np.ascontiguousarray(spec, dtype=np.complex128)
+    rows = int(np.prod(spec.shape[:-1]))
+    out = np.zeros(rows)
+    _check(lib().or_range_peaks(spec.ctypes.data, rows, spec.shape[-1], os_range, out.ctypes.data))
+    return out.reshape(spec.shape[:-1])
+
+
+def multilaterate(scene, rhat: np.ndarray, threads: int | None = None):
+    """multilaterate_location (src/indirect.cpp:58-83): (idx [T], residual [T])."""
+    rhat = np.ascontiguousarray(rhat, dtype=np.float64)
+    T = rhat.shape[0]
+    idx = np.zeros(T, dtype=np.int64)
+    res = np.zeros(T)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().or_multilaterate(C.byref(w), C.byref(g), rhat.ctypes.data, T, threads or nthreads(),
+                                  idx.ctypes.data, res.ctypes.data))
+    return idx, res
 
 
 def topk_local_max(scene, m: np.ndarray, k: int):

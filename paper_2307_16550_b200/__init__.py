@@ -13,7 +13,8 @@ from .api import (Context, HopTable, InvalidArgument, GridhopRuntimeError, Domai
                   hop_decision_map, hop_argmax, hop_estimate, campaign_hop, hop_topk,
                   campaign_hop_topk, topk_local_max,
                   location_decision_map, direct_argmax, argmax_index, lib, exported_symbols,
-                  scene_hash, ght1_write, ght1_read, table_save, table_load)
+                  scene_hash, ght1_write, ght1_read, table_save, table_load,
+                  indirect_argmin, multilaterate)
 
 __all__ = [
     "scene", "Scene", "baseline", "small", "Context", "HopTable", "InvalidArgument",
@@ -22,4 +23,5 @@ __all__ = [
     "hop_estimate", "campaign_hop", "location_decision_map", "direct_argmax", "argmax_index",
     "lib", "exported_symbols", "precompute_hop_table_shard", "hop_topk", "campaign_hop_topk",
     "topk_local_max", "scene_hash", "ght1_write", "ght1_read", "table_save", "table_load",
+    "indirect_argmin", "multilaterate",
 ]

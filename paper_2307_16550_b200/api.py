@@ -100,6 +100,8 @@ def lib() -> C.CDLL:
             "gh_direct_map_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp]),
             "gh_direct_argmax_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp, vp]),
             "gh_scene_hash": (u64, [i32, i32, i32, f64, f64, f64, vp, vp]),
+            "gh_indirect_argmin_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, vp, vp, vp]),
+            "gh_multilaterate_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, vp, vp]),
             "gh_ght1_write": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp]),
             "gh_ght1_read": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp, i64]),
             "gh_table_save": (C.c_int, [vp, C.c_char_p, u64]),
@@ -274,6 +276,36 @@ def upload_hop_table(ctx: Context, scene: Scene, scheme: int, idx: np.ndarray,
     _check(lib().gh_table_upload(ctx.h, C.byref(w), C.byref(g), scheme, idx.ctypes.data, cptr,
                                  C.byref(h)))
     return HopTable(ctx, scene, h)
+
+
+def indirect_argmin(ctx: Context, scene: Scene, frames):
+    """Indirect pipeline location stage (src/indirect.cpp:10-83, Mc = 1):
+    (r_hat fp64 [T, P], bin int64 [T], residual fp64 [T])."""
+    torch = _torch()
+    frames = _as_float_frames(frames)
+    T = frames.shape[0]
+    dev = frames.device
+    rhat = torch.empty((T, scene.n_pairs), dtype=torch.float64, device=dev)
+    idx = torch.empty(T, dtype=torch.int64, device=dev)
+    res = torch.empty(T, dtype=torch.float64, device=dev)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_indirect_argmin_d(ctx.h, C.byref(w), C.byref(g), _ptr(frames), T, _ptr(rhat),
+                                      _ptr(idx), _ptr(res)))
+    return rhat, idx, res
+
+
+def multilaterate(ctx: Context, scene: Scene, rhat):
+    """multilaterate_location (src/indirect.cpp:58-83) on device range
+    estimates rhat fp64 [T, P]: (bin int64 [T], residual fp64 [T])."""
+    torch = _torch()
+    rhat = rhat.contiguous()
+    T = rhat.shape[0]
+    idx = torch.empty(T, dtype=torch.int64, device=rhat.device)
+    res = torch.empty(T, dtype=torch.float64, device=rhat.device)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().gh_multilaterate_d(ctx.h, C.byref(w), C.byref(g), _ptr(rhat), T, _ptr(idx),
+                                    _ptr(res)))
+    return idx, res
 
 
 def scene_hash(n_chirps: int, n_samples: int, f0: float, bandwidth: float,

@@ -385,6 +385,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->mapbuf.release();
     c->seeds.release();
     c->amax.release();
+    c->misc2.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)
@@ -949,6 +950,56 @@ int gh_table_load(gh_ctx* ctx, const char* path, const gh_wave* wave, const gh_g
     if (st != GH_OK) fail(st, g_err);
     reinterpret_cast<gh::Table*>(t)->max_residual = h.max_residual;
     *out = t;
+  });
+}
+
+int gh_multilaterate_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                       const double* rhat_d, int32_t n_trials, int64_t* idx_d, double* res_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!rhat_d || !idx_d || !res_d)))
+      fail(GH_EINVAL, "multilateration: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    gh::launch_multilaterate(c, tr, wave, grid, rhat_d, n_trials, idx_d, res_d);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    txrx.release();
+  });
+}
+
+int gh_indirect_argmin_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                         const float* frames_d, int32_t n_trials, double* rhat_d, int64_t* idx_d,
+                         double* res_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!frames_d || !idx_d || !res_d)))
+      fail(GH_EINVAL, "indirect: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    const int P = wave->n_pairs, N = wave->n_samples, M = N * wave->os_range;
+    const int64_t rows = (int64_t)n_trials * P;
+    // natural complex spectra [T][P][M], then r_hat [T][P] (caller's or scratch)
+    const size_t spec_bytes = sizeof(float2) * rows * M;
+    auto* base = static_cast<unsigned char*>(
+        c->spectra.get(spec_bytes + (rhat_d ? 0 : sizeof(double) * rows)));
+    auto* spec = reinterpret_cast<float2*>(base);
+    double* rh = rhat_d ? rhat_d : reinterpret_cast<double*>(base + spec_bytes);
+    gh::launch_fft(c, reinterpret_cast<const float2*>(frames_d), nullptr, n_trials, P, N,
+                   wave->os_range, 16, gh::FFT_NATURAL, spec);
+    gh::launch_range_peaks(c, spec, rows, M, wave->os_range, rh);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    gh::launch_multilaterate(c, tr, wave, grid, rh, n_trials, idx_d, res_d);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    txrx.release();
   });
 }
 

@@ -61,7 +61,7 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2;
   int twiddle_m = 0;
   int direct_impl = 0;  // 0: tcgen05 3xFP16, 1: CUDA-core fp32, 2: tcgen05 v1, 3: tcgen05 3xTF32
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
@@ -229,6 +229,11 @@ void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
 void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
                  int64_t* idx_d,
                  float* val_d);
+// indirect pipeline, location stage (gh_indirect.cu)
+void launch_range_peaks(Ctx* ctx, const float2* spec_d, int64_t rows, int M, int os,
+                        double* rhat_d);
+void launch_multilaterate(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                          const double* rhat_d, int T, int64_t* idx_d, double* res_d);
 void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const float2* frames_d, int T, int combine, float* map_d,
                      unsigned long long* keys_d);
