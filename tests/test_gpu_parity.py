@@ -141,6 +141,22 @@ def test_hop_estimate_host_buffers(ctx, small_scene):
         gh.hop_estimate(ctx, t, fr[:, :2])
 
 
+def test_hop_estimate_pipelined_chunks(ctx, small_scene):
+    # >= 1024 trials: the host entry point pipelines H2D copies of ragged
+    # trial chunks over two streams; results must equal the device path
+    sc = small_scene
+    T = 1029
+    fr, _ = O.synth(sc, 7, T)
+    t = gh.precompute_hop_table(ctx, sc)
+    idx, val = gh.hop_estimate(ctx, t, fr)
+    d_idx, d_val = gh.hop_argmax(ctx, t, frames_to_dev(fr))
+    assert np.array_equal(idx, d_idx.cpu().numpy())
+    assert np.array_equal(val, d_val.cpu().numpy().astype(np.float64))
+    # and a second call reusing the context's buffers and events
+    idx2, _ = gh.hop_estimate(ctx, t, fr[:1030 - 6])
+    assert np.array_equal(idx2, idx[:1024])
+
+
 def test_campaign_matches_oracle_campaign(ctx):
     sc = S.baseline("c1")
     T = 64
