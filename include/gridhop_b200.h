@@ -140,6 +140,41 @@ int gh_table_info(const gh_table* t, int64_t* n_bins, int32_t* n_pairs,
 int gh_table_download(gh_table* t, uint32_t* idx, double* coef);
 int gh_table_destroy(gh_table* t);
 
+/* ---- MRF1 capture container ---------------------------------------------
+ * write_frames / read_frames (src/frame_io.cpp:53-164, format
+ * include/gridhop/frame_io.hpp:10-16): little-endian "MRF1", u32 version (1)
+ * / Q / Mc / Ms / frame count, f64 f0 / bandwidth / chirp duration, (Q+1)
+ * coordinate pairs (TX first), then frames receiver-major, each matrix
+ * row-major, entries as (re, im) f64 — i.e. complex128 [T][Q][Mc][Ms].
+ * Validation errors are GH_EINVAL with the reference's texts ("waveform:
+ * n_chirps must be >= 2", ...); file errors GH_ERUNTIME ("<path>: bad magic
+ * (not an MRF1 capture)", "<path>: payload size mismatch ...", ...).
+ * gh_mrf1_read with rx_xy = frames = NULL reads the header only. */
+typedef struct gh_mrf1_header {
+  int32_t n_rx;
+  int32_t n_chirps;
+  int32_t n_samples;
+  int32_t n_frames;
+  double f0;
+  double bandwidth;
+  double chirp_duration;
+  double tx[2];
+} gh_mrf1_header;
+int gh_mrf1_write(const char* path, const gh_mrf1_header* hdr, const double* rx_xy,
+                  const double* frames);
+int gh_mrf1_read(const char* path, gh_mrf1_header* hdr, double* rx_xy, int32_t rx_capacity,
+                 double* frames, int64_t capacity);
+
+/* ---- multi-chirp frames (the reference's slow-time axis, Mc > 1) --------
+ * scan_planes / hop_bin_value over Mc chirps (src/hopping.cpp:59-117):
+ * value(bin) = sum_q sum_mc |Z_q(mc, I(bin, q))|^2 for K = 1 (nearest)
+ * tables, power combine. frames complex64 [T][P][Mc][N] (a FrameSet per
+ * trial, receiver-major, each matrix row-major); map fp32 [T][G]. */
+int gh_hop_map_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                    int32_t n_chirps, float* map_d);
+int gh_hop_argmax_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                       int32_t n_chirps, int64_t* idx_d, float* val_d);
+
 /* ---- indirect pipeline, location stage ---------------------------------
  * range_doppler_map + RangeDopplerMap::peak + multilaterate_location
  * (src/indirect.cpp:10-83) at Mc = 1: per (trial, pair) r_hat = (first

@@ -755,6 +755,37 @@ int or_hop_map(const double* spectra, int32_t n_trials, int32_t n_pairs, int32_t
   });
 }
 
+// scan_planes / hop_bin_value over Mc chirps (hopping.cpp:59-117): the
+// reference's slow-time axis, value(bin) = sum_q sum_mc |sum_j c_j Z_q(mc, I_j)|^2
+// (pairs outer, chirps inner). spectra [T][P][Mc][M][2], power combine.
+int or_hop_map_mc(const double* spectra, int32_t n_trials, int32_t n_pairs, int32_t n_chirps,
+                  int32_t m, const uint32_t* idx, const double* coef, int64_t n_bins, int32_t k,
+                  double* map) {
+  return guarded([&] {
+    if (k < 1 || k > 3) throw std::invalid_argument("hop: unsupported interpolation order");
+    const auto* sp = reinterpret_cast<const cplx*>(spectra);
+    for (int32_t t = 0; t < n_trials; ++t)
+      for (int64_t b = 0; b < n_bins; ++b) {
+        double value = 0.0;
+        for (int p = 0; p < n_pairs; ++p) {
+          const size_t at = (static_cast<size_t>(b) * n_pairs + p) * k;
+          for (int mc = 0; mc < n_chirps; ++mc) {
+            const cplx* z = sp + ((static_cast<size_t>(t) * n_pairs + p) * n_chirps + mc) * m;
+            double vr = 0.0, vi = 0.0;
+            for (int j = 0; j < k; ++j) {
+              const double cr = coef[2 * (at + j)], ci = coef[2 * (at + j) + 1];
+              const cplx zz = z[idx[at + j]];
+              vr = vr + cr * zz.real() - ci * zz.imag();
+              vi = vi + cr * zz.imag() + ci * zz.real();
+            }
+            value += vr * vr + vi * vi;
+          }
+        }
+        map[static_cast<size_t>(t) * n_bins + b] = value;
+      }
+  });
+}
+
 int or_direct_map(const double* frames, int32_t n_trials, const or_wave* w,
                   const or_grid* g, int magnitude, int n_threads, double* map) {
   return guarded([&] {

@@ -97,6 +97,9 @@ int or_spectra(const double* frames, int64_t rows, int32_t n, int32_t m,
 int or_hop_map(const double* spectra, int32_t n_trials, int32_t n_pairs,
                int32_t m, const uint32_t* idx, const double* coef,
                int64_t n_bins, int32_t k, int magnitude, double* map);
+int or_hop_map_mc(const double* spectra, int32_t n_trials, int32_t n_pairs, int32_t n_chirps,
+                  int32_t m, const uint32_t* idx, const double* coef, int64_t n_bins, int32_t k,
+                  double* map);
 int or_direct_map(const double* frames, int32_t n_trials, const or_wave* w,
                   const or_grid* g, int magnitude, int n_threads, double* map);
 int64_t or_argmax(const double* v, int64_t n);

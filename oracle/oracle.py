@@ -58,6 +58,7 @@ def lib():
             "or_argmax": (i64, [vp, i64]),
             "or_topk_local_max": (C.c_int, [vp, P(CGrid), i32, vp, vp]),
             "or_range_peaks": (C.c_int, [vp, i64, i32, i32, vp]),
+            "or_hop_map_mc": (C.c_int, [vp, i32, i32, i32, i32, vp, vp, i64, i32, vp]),
             "or_multilaterate": (C.c_int, [P(CWave), P(CGrid), vp, i32, C.c_int, vp, vp]),
             "or_campaign_hop": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), vp, vp, i32, C.c_int,
                                           C.c_int, u64, i32, C.c_int, vp, vp]),
@@ -152,6 +153,19 @@ def hop_map(spec: np.ndarray, idx: np.ndarray, coef: np.ndarray, magnitude: bool
     out = np.zeros((T, G))
     _check(lib().or_hop_map(spec.ctypes.data, T, P, M, idx.ctypes.data, coef.ctypes.data, G, K,
                             int(magnitude), out.ctypes.data))
+    return out
+
+
+def hop_map_mc(spec: np.ndarray, idx: np.ndarray, coef: np.ndarray):
+    """scan_planes over Mc chirps (power): spec complex [T, P, Mc, M]."""
+    spec = np.ascontiguousarray(spec, dtype=np.complex128)
+    T, P, Mc, M = spec.shape
+    G, P2, K = idx.shape
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    coef = np.ascontiguousarray(coef, dtype=np.complex128)
+    out = np.zeros((T, G))
+    _check(lib().or_hop_map_mc(spec.ctypes.data, T, P, Mc, M, idx.ctypes.data, coef.ctypes.data, G, K,
+                               out.ctypes.data))
     return out
 
 

@@ -45,6 +45,13 @@ class CudaError(RuntimeError):
 _EXC = {1: InvalidArgument, 2: GridhopRuntimeError, 3: DomainError, 4: CudaError}
 
 
+class Mrf1Header(C.Structure):
+    """gh_mrf1_header: the MRF1 capture header (frame_io.hpp:10-16)."""
+    _fields_ = [("n_rx", C.c_int32), ("n_chirps", C.c_int32), ("n_samples", C.c_int32),
+                ("n_frames", C.c_int32), ("f0", C.c_double), ("bandwidth", C.c_double),
+                ("chirp_duration", C.c_double), ("tx", C.c_double * 2)]
+
+
 class Ght1Header(C.Structure):
     """gh_ght1_header: the GHT1 container header (interp.hpp:69-71)."""
     _fields_ = [("n_pairs", C.c_int32), ("n_bins", C.c_int32), ("k", C.c_int32),
@@ -101,6 +108,10 @@ def lib() -> C.CDLL:
             "gh_direct_argmax_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, i32, vp, vp]),
             "gh_scene_hash": (u64, [i32, i32, i32, f64, f64, f64, vp, vp]),
             "gh_indirect_argmin_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, vp, vp, vp]),
+            "gh_hop_map_mc_d": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+            "gh_hop_argmax_mc_d": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
+            "gh_mrf1_write": (C.c_int, [C.c_char_p, P(Mrf1Header), vp, vp]),
+            "gh_mrf1_read": (C.c_int, [C.c_char_p, P(Mrf1Header), vp, i32, vp, i64]),
             "gh_multilaterate_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, vp, vp]),
             "gh_ght1_write": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp]),
             "gh_ght1_read": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp, i64]),
@@ -276,6 +287,66 @@ def upload_hop_table(ctx: Context, scene: Scene, scheme: int, idx: np.ndarray,
     _check(lib().gh_table_upload(ctx.h, C.byref(w), C.byref(g), scheme, idx.ctypes.data, cptr,
                                  C.byref(h)))
     return HopTable(ctx, scene, h)
+
+
+def _as_float_frames_mc(frames):
+    torch = _torch()
+    if frames.dtype != torch.complex64 or not frames.is_cuda or not frames.is_contiguous():
+        raise InvalidArgument("frames must be a contiguous CUDA complex64 tensor [T, P, Mc, N]")
+    return frames
+
+
+def hop_map_mc(ctx: Context, table: HopTable, frames):
+    """scan_planes over Mc chirps (src/hopping.cpp:59-117), K = 1 tables:
+    frames complex64 [T, P, Mc, N] -> map fp32 [T, G]."""
+    torch = _torch()
+    frames = _as_float_frames_mc(frames)
+    T, P, Mc, N = frames.shape
+    if P != table.n_pairs or N != table.scene.n_samples:
+        raise InvalidArgument("hop: frame shape mismatch")
+    out = torch.empty((T, table.n_bins), dtype=torch.float32, device=frames.device)
+    _check(lib().gh_hop_map_mc_d(ctx.h, table.h, _ptr(frames), T, Mc, _ptr(out)))
+    return out
+
+
+def hop_argmax_mc(ctx: Context, table: HopTable, frames):
+    """hop_estimate's location stage on multi-chirp frames [T, P, Mc, N]."""
+    torch = _torch()
+    frames = _as_float_frames_mc(frames)
+    T, P, Mc, N = frames.shape
+    if P != table.n_pairs or N != table.scene.n_samples:
+        raise InvalidArgument("hop: frame shape mismatch")
+    idx = torch.empty(T, dtype=torch.int64, device=frames.device)
+    val = torch.empty(T, dtype=torch.float32, device=frames.device)
+    _check(lib().gh_hop_argmax_mc_d(ctx.h, table.h, _ptr(frames), T, Mc, _ptr(idx), _ptr(val)))
+    return idx, val
+
+
+def mrf1_write(path, frames: np.ndarray, f0: float, bandwidth: float, chirp_duration: float,
+               tx_xy, rx_xy) -> None:
+    """write_frames (src/frame_io.cpp:53-100): frames complex128 [T, Q, Mc, Ms]."""
+    frames = np.ascontiguousarray(frames, dtype=np.complex128)
+    T, Q, Mc, Ms = frames.shape
+    rx = np.ascontiguousarray(rx_xy, dtype=np.float64).reshape(-1, 2)
+    if rx.shape[0] != Q:
+        raise InvalidArgument(f"{path}: frame/receiver count mismatch")
+    h = Mrf1Header(Q, Mc, Ms, T, f0, bandwidth, chirp_duration, (C.c_double * 2)(*tx_xy))
+    _check(lib().gh_mrf1_write(str(path).encode(), C.byref(h), rx.ctypes.data,
+                               frames.ctypes.data if T else None))
+
+
+def mrf1_read(path):
+    """read_frames (src/frame_io.cpp:102-164): (header dict, rx [Q, 2],
+    frames complex128 [T, Q, Mc, Ms])."""
+    h = Mrf1Header()
+    _check(lib().gh_mrf1_read(str(path).encode(), C.byref(h), None, 0, None, 0))
+    rx = np.empty((h.n_rx, 2))
+    frames = np.empty((h.n_frames, h.n_rx, h.n_chirps, h.n_samples), dtype=np.complex128)
+    _check(lib().gh_mrf1_read(str(path).encode(), C.byref(h), rx.ctypes.data, h.n_rx,
+                              frames.ctypes.data, frames.size))
+    hdr = {f: getattr(h, f) for f, _ in Mrf1Header._fields_ if f != "tx"}
+    hdr["tx"] = (h.tx[0], h.tx[1])
+    return hdr, rx, frames
 
 
 def indirect_argmin(ctx: Context, scene: Scene, frames):

@@ -204,6 +204,43 @@ void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthPar
   }
 }
 
+// Multi-chirp location stage (Mc > 1, scan_planes over the slow-time axis,
+// hopping.cpp:59-117) for K = 1 tables: per trial chunk, natural spectra of
+// every chirp, their power summed over chirps in the gather layout, then the
+// unchanged gather (map mode or fused argmax). Chunks keep the natural
+// spectra scratch under 4 GiB.
+void hop_mc(gh::Ctx* c, gh::Table* t, const float2* frames, int T, int Mc, float* map_d,
+            int64_t* idx_d, float* val_d) {
+  if (t->K != 1)
+    fail(GH_EINVAL, "hop: multi-chirp frames need a K = 1 (nearest) table");
+  gh::build_plan(c, t);
+  const gh::Plan& pl = t->plan;
+  const int64_t per_trial = (int64_t)t->P * Mc * t->M;  // complex64 spectra
+  int64_t chunk = (int64_t(1) << 29) / std::max<int64_t>(per_trial, 1);
+  chunk = std::max<int64_t>(pl.tb, chunk / pl.tb * pl.tb);
+  chunk = std::min<int64_t>(chunk, (T + pl.tb - 1) / pl.tb * pl.tb);
+  const size_t nat_bytes = sizeof(float2) * per_trial * chunk;
+  const size_t pw_bytes = sizeof(float) * (size_t)((chunk + pl.tb - 1) / pl.tb) * pl.tb * t->P * t->M;
+  auto* base = static_cast<unsigned char*>(c->spectra.get(nat_bytes + pw_bytes));
+  auto* nat = reinterpret_cast<float2*>(base);
+  auto* pw = reinterpret_cast<float*>(base + nat_bytes);
+  unsigned long long* keys = nullptr;
+  if (!map_d) {
+    keys = static_cast<unsigned long long*>(c->keys.get(sizeof(unsigned long long) * T));
+    GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * T, c->stream));
+  }
+  for (int t0 = 0; t0 < T; t0 += static_cast<int>(chunk)) {
+    const int tc = static_cast<int>(std::min<int64_t>(chunk, T - t0));
+    // frames [tc][P][Mc][N] are [tc][P*Mc][N]: natural spectra [tc][P][Mc][M]
+    gh::launch_fft(c, frames + (int64_t)t0 * t->P * Mc * t->N, nullptr, tc, t->P * Mc, t->N,
+                   t->os, 16, gh::FFT_NATURAL, nat);
+    gh::launch_chirp_power(c, nat, tc, t->P, Mc, t->M, pl.tb, pw);
+    gh::launch_gather(c, t, pw, tc, GH_POWER, map_d ? map_d + (int64_t)t0 * t->G : nullptr,
+                      keys ? keys + t0 : nullptr);
+  }
+  if (!map_d) gh::launch_decode_keys(c, keys, T, idx_d, val_d);
+}
+
 __global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -328,6 +365,34 @@ void ght1_read(const std::string& path, gh_ght1_header& h, uint32_t* idx, double
       coef[2 * (e + j) + 1] = rd.get<double>("coefficient");
     }
   }
+}
+
+// ------------------------------------------------------------ MRF1 capture
+// Restates write_frames / read_frames (src/frame_io.cpp:53-164) and the
+// WaveformConfig / SceneGeometry validation they run (model.cpp:19-43).
+constexpr uint32_t kMrf1Version = 1;
+
+void mrf1_validate(const gh_mrf1_header& h, const double* rx) {
+  auto check = [](bool ok, const char* what) {
+    if (!ok) fail(GH_EINVAL, what);
+  };
+  check(std::isfinite(h.f0) && h.f0 > 0.0, "waveform: f0 must be positive");
+  check(std::isfinite(h.bandwidth) && h.bandwidth > 0.0, "waveform: bandwidth must be positive");
+  check(std::isfinite(h.chirp_duration) && h.chirp_duration > 0.0,
+        "waveform: chirp_duration must be positive");
+  check(h.n_chirps >= 2, "waveform: n_chirps must be >= 2");
+  check(h.n_samples >= 2, "waveform: n_samples must be >= 2");
+  check(h.n_rx >= 2, "geometry: at least two receivers required");
+  for (int i = 0; i < h.n_rx; ++i) {
+    check(std::isfinite(rx[2 * i]) && std::isfinite(rx[2 * i + 1]),
+          "geometry: receiver position must be finite");
+    if (std::hypot(rx[2 * i] - h.tx[0], rx[2 * i + 1] - h.tx[1]) == 0.0)
+      fail(GH_EINVAL, "geometry: receiver coincides with TX");
+    for (int j = i + 1; j < h.n_rx; ++j)
+      if (std::hypot(rx[2 * i] - rx[2 * j], rx[2 * i + 1] - rx[2 * j + 1]) == 0.0)
+        fail(GH_EINVAL, "geometry: receivers coincide");
+  }
+  check(std::isfinite(h.tx[0]) && std::isfinite(h.tx[1]), "geometry: TX position must be finite");
 }
 
 // scene_hash (src/model.cpp:135-166), including the reference's offset basis
@@ -1000,6 +1065,119 @@ int gh_indirect_argmin_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
     gh::launch_multilaterate(c, tr, wave, grid, rh, n_trials, idx_d, res_d);
     GH_CUDA(cudaStreamSynchronize(c->stream));
     txrx.release();
+  });
+}
+
+int gh_hop_map_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                    int32_t n_chirps, float* map_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!frames_d || !map_d))) fail(GH_EINVAL, "hop: null argument");
+    if (n_chirps < 1) fail(GH_EINVAL, "waveform: n_chirps must be >= 1");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    hop_mc(c, t, reinterpret_cast<const float2*>(frames_d), n_trials, n_chirps, map_d, nullptr,
+           nullptr);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_hop_argmax_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
+                       int32_t n_chirps, int64_t* idx_d, float* val_d) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!frames_d || !idx_d || !val_d)))
+      fail(GH_EINVAL, "hop: null argument");
+    if (n_chirps < 1) fail(GH_EINVAL, "waveform: n_chirps must be >= 1");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    hop_mc(c, t, reinterpret_cast<const float2*>(frames_d), n_trials, n_chirps, nullptr, idx_d,
+           val_d);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_mrf1_write(const char* path, const gh_mrf1_header* hdr, const double* rx_xy,
+                  const double* frames) {
+  return guarded([&] {
+    if (!path || !hdr || !rx_xy || (hdr->n_frames > 0 && !frames))
+      fail(GH_EINVAL, "capture: null argument");
+    if (hdr->n_frames < 0) fail(GH_EINVAL, "capture: frame count must be >= 0");
+    mrf1_validate(*hdr, rx_xy);
+    const size_t samples = (size_t)hdr->n_frames * hdr->n_rx * hdr->n_chirps * hdr->n_samples;
+    std::string out;
+    out.reserve(24 + 24 + (size_t)(hdr->n_rx + 1) * 16 + samples * 16);
+    out.append("MRF1", 4);
+    ght1_put<uint32_t>(out, kMrf1Version);
+    ght1_put<uint32_t>(out, (uint32_t)hdr->n_rx);
+    ght1_put<uint32_t>(out, (uint32_t)hdr->n_chirps);
+    ght1_put<uint32_t>(out, (uint32_t)hdr->n_samples);
+    ght1_put<uint32_t>(out, (uint32_t)hdr->n_frames);
+    ght1_put<double>(out, hdr->f0);
+    ght1_put<double>(out, hdr->bandwidth);
+    ght1_put<double>(out, hdr->chirp_duration);
+    ght1_put<double>(out, hdr->tx[0]);
+    ght1_put<double>(out, hdr->tx[1]);
+    for (int q = 0; q < hdr->n_rx; ++q) {
+      ght1_put<double>(out, rx_xy[2 * q]);
+      ght1_put<double>(out, rx_xy[2 * q + 1]);
+    }
+    // frames receiver-major, each matrix row-major: exactly [T][Q][Mc][Ms]
+    out.append(reinterpret_cast<const char*>(frames), samples * 16);
+    std::ofstream f(path, std::ios::binary | std::ios::trunc);
+    if (!f) fail(GH_ERUNTIME, std::string(path) + ": cannot open for writing");
+    f.write(out.data(), static_cast<std::streamsize>(out.size()));
+    f.flush();
+    if (!f) fail(GH_ERUNTIME, std::string(path) + ": short write");
+  });
+}
+
+int gh_mrf1_read(const char* path, gh_mrf1_header* hdr, double* rx_xy, int32_t rx_capacity,
+                 double* frames, int64_t capacity) {
+  return guarded([&] {
+    if (!path || !hdr) fail(GH_EINVAL, "capture: null argument");
+    const std::string p(path);
+    const std::string data = ght1_read_file(p);
+    Ght1Reader rd{data.data(), data.size(), p};
+    rd.need(4, "magic");
+    if (std::memcmp(rd.p, "MRF1", 4) != 0)
+      fail(GH_ERUNTIME, p + ": bad magic (not an MRF1 capture)");
+    rd.p += 4;
+    rd.left -= 4;
+    const uint32_t version = rd.get<uint32_t>("version");
+    if (version != kMrf1Version)
+      fail(GH_ERUNTIME, p + ": unsupported capture version " + std::to_string(version));
+    gh_mrf1_header h{};
+    h.n_rx = (int32_t)rd.get<uint32_t>("receiver count");
+    h.n_chirps = (int32_t)rd.get<uint32_t>("chirp count");
+    h.n_samples = (int32_t)rd.get<uint32_t>("sample count");
+    h.n_frames = (int32_t)rd.get<uint32_t>("frame count");
+    h.f0 = rd.get<double>("carrier");
+    h.bandwidth = rd.get<double>("bandwidth");
+    h.chirp_duration = rd.get<double>("chirp duration");
+    h.tx[0] = rd.get<double>("TX coordinate");
+    h.tx[1] = rd.get<double>("TX coordinate");
+    std::vector<double> rx(2 * (size_t)(uint32_t)h.n_rx);
+    for (size_t q = 0; q < rx.size(); ++q) rx[q] = rd.get<double>("RX coordinate");
+    mrf1_validate(h, rx.data());
+    const size_t samples = (size_t)(uint32_t)h.n_frames * (uint32_t)h.n_rx * (uint32_t)h.n_chirps *
+                           (uint32_t)h.n_samples;
+    if (rd.left != samples * 16)
+      fail(GH_ERUNTIME, p + ": payload size mismatch (expected " + std::to_string(samples * 16) +
+                            " bytes, have " + std::to_string(rd.left) + ")");
+    *hdr = h;
+    if (rx_xy) {
+      if (rx_capacity < h.n_rx) fail(GH_EINVAL, "capture: receiver array too small");
+      std::memcpy(rx_xy, rx.data(), sizeof(double) * rx.size());
+    }
+    if (frames) {
+      if (capacity < (int64_t)samples) fail(GH_EINVAL, "capture: frame array too small");
+      std::memcpy(frames, rd.p, samples * 16);
+    }
   });
 }
 

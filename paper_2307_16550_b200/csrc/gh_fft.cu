@@ -854,6 +854,53 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   GH_LAUNCHED(ctx);
 }
 
+namespace {
+
+// Multi-chirp frames (the reference's slow-time axis, Mc > 1): power summed
+// over a trial's chirps, sum_mc |Z_q(mc, k)|^2, written in the gather layout
+// [batch][pair][M][TB]. A CTA owns (batch, pair, 64 range bins): it reads the
+// natural spectra [T][P][Mc][M] with consecutive threads on consecutive bins
+// (coalesced), accumulates in shared memory and stores each bin's TB-run
+// contiguously. K = 1 tables only: the nearest atom's value is then exactly
+// this chirp sum (hopping.cpp:92-99 with c = 1).
+constexpr int kCpBins = 64;
+
+__global__ void k_chirp_power(const float2* __restrict__ spec, int T, int P, int Mc, int M,
+                              int tb, float* __restrict__ out) {
+  extern __shared__ float pw[];  // [kCpBins][tb]
+  const int batch = blockIdx.z, p = blockIdx.y, k0 = blockIdx.x * kCpBins;
+  for (int e = threadIdx.x; e < kCpBins * tb; e += blockDim.x) {
+    const int r = e / kCpBins, k = e % kCpBins;  // k fastest: coalesced reads
+    const int t = batch * tb + r;
+    float acc = 0.f;
+    if (t < T && k0 + k < M) {
+      const float2* z = spec + (((int64_t)t * P + p) * Mc) * M + k0 + k;
+      for (int mc = 0; mc < Mc; ++mc) {
+        const float2 v = z[(int64_t)mc * M];
+        acc += v.x * v.x + v.y * v.y;
+      }
+    }
+    pw[k * tb + r] = acc;
+  }
+  __syncthreads();
+  float* dst = out + (((int64_t)batch * P + p) * M + k0) * tb;
+  const int n = (M - k0 < kCpBins ? M - k0 : kCpBins) * tb;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = pw[e];
+}
+
+}  // namespace
+
+void launch_chirp_power(Ctx* ctx, const float2* spec_d, int T, int P, int Mc, int M, int tb,
+                        float* out_d) {
+  const int n_tb = (T + tb - 1) / tb;
+  if (n_tb > 65535) fail(GH_EINVAL, "spectra: too many trial batches for one launch");
+  dim3 grid((M + kCpBins - 1) / kCpBins, P, n_tb);
+  KTimer kt(ctx, "chirp_power");
+  k_chirp_power<<<grid, 256, sizeof(float) * kCpBins * tb, ctx->stream>>>(spec_d, T, P, Mc, M, tb,
+                                                                          out_d);
+  GH_LAUNCHED(ctx);
+}
+
 void launch_synth(Ctx* ctx, const SynthParams& sp, int T, int P, int N, float2* frames_d,
                   double* truth_d) {
   if (sp.camp.n_targets < 1 || sp.camp.n_targets > kMaxTargets)

@@ -218,6 +218,10 @@ enum FftOut { FFT_NATURAL = 0, FFT_GATHER_POWER = 1, FFT_GATHER_MAG = 2, FFT_GAT
 
 void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth,
                 int T, int P, int N, int os, int tb, int out_kind, void* out_d);
+// multi-chirp frames: natural spectra [T][P][Mc][M] -> chirp-summed power in
+// the gather layout [batch][pair][M][tb]
+void launch_chirp_power(Ctx* ctx, const float2* spec_d, int T, int P, int Mc, int M, int tb,
+                        float* out_d);
 void launch_synth(Ctx* ctx, const SynthParams& sp, int T, int P, int N, float2* frames_d,
                   double* truth_d);
 void build_table_device(Ctx* ctx, Table* t, int wrap);
