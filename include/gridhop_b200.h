@@ -175,6 +175,30 @@ int gh_hop_map_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t
 int gh_hop_argmax_mc_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_trials,
                        int32_t n_chirps, int64_t* idx_d, float* val_d);
 
+/* ---- velocity stage at the located bins ----------------------------------
+ * hop_velocity (src/hopping.cpp:185-236) and direct_velocity
+ * (src/direct.cpp:145-228) for T trials of multi-chirp frames, each at its
+ * located bin loc_d[t] (e.g. from gh_hop_argmax_mc_d): range compression at
+ * x_hat, then the velocity-grid scan — hop: nearest bins of the zero-padded
+ * slow-time spectrum (n_d = os_doppler * Mc; Mc and os_doppler powers of
+ * two); direct: exact correlation with each pair's Doppler atom. The grid is
+ * VelocityGrid (model.hpp:93-107): point k = spacing * (k % n - half,
+ * k / n - half), n = 2 half + 1; first maximum wins. frames complex64
+ * [T][P][Mc][N]; out velocity-grid index int64 [T] and value fp32 [T]. */
+typedef struct gh_velocity_grid {
+  double doppler_scale;  /* WaveformConfig::doppler_scale = f0 Tc Mc / c   */
+  double spacing;        /* VelocityGrid::spacing, m/s                     */
+  int32_t half;          /* VelocityGrid::half                             */
+  int32_t os_doppler;    /* hop: slow-time zero padding (>= 1)             */
+} gh_velocity_grid;
+int gh_hop_velocity_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                      const gh_velocity_grid* vgrid, const float* frames_d, int32_t n_trials,
+                      int32_t n_chirps, const int64_t* loc_d, int64_t* vidx_d, float* vval_d);
+int gh_direct_velocity_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                         const gh_velocity_grid* vgrid, const float* frames_d,
+                         int32_t n_trials, int32_t n_chirps, const int64_t* loc_d,
+                         int64_t* vidx_d, float* vval_d);
+
 /* ---- indirect pipeline, location stage ---------------------------------
  * range_doppler_map + RangeDopplerMap::peak + multilaterate_location
  * (src/indirect.cpp:10-83) at Mc = 1: per (trial, pair) r_hat = (first

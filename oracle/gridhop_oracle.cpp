@@ -865,6 +865,149 @@ int or_multilaterate(const or_wave* w, const or_grid* g, const double* rhat, int
   });
 }
 
+// ---------------------------------------------------------------- velocity
+// VelocityGrid (model.hpp:93-107, model.cpp:116-131): point k =
+// spacing * (k % n - half, k / n - half), n = 2 half + 1 (2-D, z = 0).
+static void velocity_point(double spacing, int half, int64_t k, double* v) {
+  const int64_t n = 2 * static_cast<int64_t>(half) + 1;
+  v[0] = spacing * static_cast<double>(k % n - half);
+  v[1] = spacing * static_cast<double>(k / n - half);
+  v[2] = 0.0;
+}
+
+// doppler_scale * (unit(x - tx) + unit(x - rx)): the slow-time bins per m/s
+// of velocity along each axis (sensed_doppler, model.cpp:54-64)
+static void doppler_dirs(const double* tx, const double* rx, const double* x, double scale,
+                         double* dir) {
+  const double ftx[3] = {x[0] - tx[0], x[1] - tx[1], x[2] - tx[2]};
+  const double frx[3] = {x[0] - rx[0], x[1] - rx[1], x[2] - rx[2]};
+  const double dtx = std::sqrt(ftx[0] * ftx[0] + ftx[1] * ftx[1] + ftx[2] * ftx[2]);
+  const double drx = std::sqrt(frx[0] * frx[0] + frx[1] * frx[1] + frx[2] * frx[2]);
+  if (dtx == 0.0 || drx == 0.0)
+    throw std::domain_error("degenerate geometry: target coincides with a station");
+  for (int d = 0; d < 3; ++d) dir[d] = scale * (ftx[d] / dtx + frx[d] / drx);
+}
+
+static double dot3(const double* a, const double* b) {
+  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// hop_velocity (hopping.cpp:185-236), batched over trials at their located
+// bins: per pair, exact range compression at x_hat with conj(range_atom),
+// the zero-padded slow-time DFT (n_d = os_d * Mc) and its power; then the
+// velocity-grid scan of nearest Doppler bins (lround, modulo n_d), first
+// maximum. frames [T][P][Mc][N][2].
+int or_hop_velocity(const double* frames, int32_t n_trials, int32_t n_chirps, const or_wave* w,
+                    const or_grid* g, double doppler_scale, double spacing, int32_t half,
+                    int32_t os_d, const int64_t* loc, int64_t* vidx, double* vval) {
+  return guarded([&] {
+    check_wave(*w);
+    if (os_d < 1) throw std::invalid_argument("hop velocity: oversampling must be >= 1");
+    if (half < 0) throw std::invalid_argument("hop velocity: empty grid");
+    const int P = w->n_pairs, N = w->n_samples, Mc = n_chirps, nd = os_d * Mc;
+    const int64_t V = (2 * static_cast<int64_t>(half) + 1) * (2 * static_cast<int64_t>(half) + 1);
+    const std::vector<cplx> tw = twiddles(nd);
+    for (int32_t t = 0; t < n_trials; ++t) {
+      double x[3];
+      grid_point(*g, loc[t], x);
+      std::vector<double> power(static_cast<size_t>(P) * nd), dirs(3 * static_cast<size_t>(P));
+      std::vector<double> h(2 * static_cast<size_t>(Mc));
+      std::vector<cplx> spec(static_cast<size_t>(nd));
+      for (int q = 0; q < P; ++q) {
+        const double r = sensed_range(w->range_scale, w->tx + 3 * q, w->rx + 3 * q, x);
+        const double* y = frames + ((static_cast<size_t>(t) * P + q) * Mc) * N * 2;
+        for (int m = 0; m < Mc; ++m) {
+          cplx acc(0.0, 0.0);
+          for (int n = 0; n < N; ++n) {
+            const cplx ca = std::conj(std::polar(1.0, kTwoPi * r / N * static_cast<double>(n)));
+            acc += cplx(y[(static_cast<size_t>(m) * N + n) * 2], y[(static_cast<size_t>(m) * N + n) * 2 + 1]) * ca;
+          }
+          h[2 * m] = acc.real();
+          h[2 * m + 1] = acc.imag();
+        }
+        dft_row(h.data(), Mc, nd, spec.data(), tw);
+        for (int i = 0; i < nd; ++i) power[static_cast<size_t>(q) * nd + i] = std::norm(spec[static_cast<size_t>(i)]);
+        doppler_dirs(w->tx + 3 * q, w->rx + 3 * q, x, doppler_scale, &dirs[3 * static_cast<size_t>(q)]);
+      }
+      int64_t best = 0;
+      double best_value = -1.0;
+      for (int64_t k = 0; k < V; ++k) {
+        double v[3];
+        velocity_point(spacing, half, k, v);
+        double value = 0.0;
+        for (int q = 0; q < P; ++q) {
+          const double u = dot3(&dirs[3 * static_cast<size_t>(q)], v);
+          const long bin = std::lround(u * static_cast<double>(os_d));
+          const int idx = static_cast<int>(((bin % nd) + nd) % nd);
+          value += power[static_cast<size_t>(q) * nd + idx];
+        }
+        if (value > best_value) {
+          best_value = value;
+          best = k;
+        }
+      }
+      vidx[t] = best;
+      vval[t] = best_value;
+    }
+  });
+}
+
+// direct_velocity (direct.cpp:145-228): range compression with conj_atom,
+// then per velocity point sum_q |sum_m h_q[m] conj(b(u_q))[m]|^2, first max.
+int or_direct_velocity(const double* frames, int32_t n_trials, int32_t n_chirps, const or_wave* w,
+                       const or_grid* g, double doppler_scale, double spacing, int32_t half,
+                       const int64_t* loc, int64_t* vidx, double* vval) {
+  return guarded([&] {
+    check_wave(*w);
+    if (half < 0) throw std::invalid_argument("velocity scan: empty grid");
+    const int P = w->n_pairs, N = w->n_samples, Mc = n_chirps;
+    const int64_t V = (2 * static_cast<int64_t>(half) + 1) * (2 * static_cast<int64_t>(half) + 1);
+    std::vector<double> cre(static_cast<size_t>(std::max(N, Mc))), cim(cre.size());
+    for (int32_t t = 0; t < n_trials; ++t) {
+      double x[3];
+      grid_point(*g, loc[t], x);
+      std::vector<cplx> h(static_cast<size_t>(P) * Mc);
+      std::vector<double> dirs(3 * static_cast<size_t>(P));
+      for (int q = 0; q < P; ++q) {
+        const double r = sensed_range(w->range_scale, w->tx + 3 * q, w->rx + 3 * q, x);
+        conj_atom(r, N, cre.data(), cim.data());
+        const double* y = frames + ((static_cast<size_t>(t) * P + q) * Mc) * N * 2;
+        for (int m = 0; m < Mc; ++m) {
+          cplx acc(0.0, 0.0);
+          for (int n = 0; n < N; ++n)
+            acc += cplx(y[(static_cast<size_t>(m) * N + n) * 2], y[(static_cast<size_t>(m) * N + n) * 2 + 1]) *
+                   cplx(cre[static_cast<size_t>(n)], cim[static_cast<size_t>(n)]);
+          h[static_cast<size_t>(q) * Mc + m] = acc;
+        }
+        doppler_dirs(w->tx + 3 * q, w->rx + 3 * q, x, doppler_scale, &dirs[3 * static_cast<size_t>(q)]);
+      }
+      int64_t best = 0;
+      double best_value = -1.0;
+      for (int64_t k = 0; k < V; ++k) {
+        double v[3];
+        velocity_point(spacing, half, k, v);
+        double value = 0.0;
+        for (int q = 0; q < P; ++q) {
+          conj_atom(dot3(&dirs[3 * static_cast<size_t>(q)], v), Mc, cre.data(), cim.data());
+          double zr = 0.0, zi = 0.0;
+          for (int m = 0; m < Mc; ++m) {
+            const cplx hm = h[static_cast<size_t>(q) * Mc + m];
+            zr += hm.real() * cre[static_cast<size_t>(m)] - hm.imag() * cim[static_cast<size_t>(m)];
+            zi += hm.real() * cim[static_cast<size_t>(m)] + hm.imag() * cre[static_cast<size_t>(m)];
+          }
+          value += zr * zr + zi * zi;
+        }
+        if (value > best_value) {
+          best_value = value;
+          best = k;
+        }
+      }
+      vidx[t] = best;
+      vval[t] = best_value;
+    }
+  });
+}
+
 int64_t or_argmax(const double* v, int64_t n) {
   int64_t r = -1;
   if (guarded([&] { r = argmax(v, n); }) != 0) return -1;

@@ -103,6 +103,14 @@ int or_hop_map_mc(const double* spectra, int32_t n_trials, int32_t n_pairs, int3
 int or_direct_map(const double* frames, int32_t n_trials, const or_wave* w,
                   const or_grid* g, int magnitude, int n_threads, double* map);
 int64_t or_argmax(const double* v, int64_t n);
+/* Velocity stage at located bins (hopping.cpp:185-236, direct.cpp:145-228):
+ * frames [T][P][Mc][N][2]; VelocityGrid (spacing, half); os_d >= 1. */
+int or_hop_velocity(const double* frames, int32_t n_trials, int32_t n_chirps, const or_wave* w,
+                    const or_grid* g, double doppler_scale, double spacing, int32_t half,
+                    int32_t os_d, const int64_t* loc, int64_t* vidx, double* vval);
+int or_direct_velocity(const double* frames, int32_t n_trials, int32_t n_chirps, const or_wave* w,
+                       const or_grid* g, double doppler_scale, double spacing, int32_t half,
+                       const int64_t* loc, int64_t* vidx, double* vval);
 /* Indirect pipeline, location stage (src/indirect.cpp:10-83, Mc = 1). */
 int or_range_peaks(const double* spectra, int64_t rows, int32_t m, int32_t os_range,
                    double* rhat);

@@ -59,6 +59,10 @@ def lib():
             "or_topk_local_max": (C.c_int, [vp, P(CGrid), i32, vp, vp]),
             "or_range_peaks": (C.c_int, [vp, i64, i32, i32, vp]),
             "or_hop_map_mc": (C.c_int, [vp, i32, i32, i32, i32, vp, vp, i64, i32, vp]),
+            "or_hop_velocity": (C.c_int, [vp, i32, i32, P(CWave), P(CGrid), f64, f64, i32, i32,
+                                          vp, vp, vp]),
+            "or_direct_velocity": (C.c_int, [vp, i32, i32, P(CWave), P(CGrid), f64, f64, i32,
+                                             vp, vp, vp]),
             "or_multilaterate": (C.c_int, [P(CWave), P(CGrid), vp, i32, C.c_int, vp, vp]),
             "or_campaign_hop": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), vp, vp, i32, C.c_int,
                                           C.c_int, u64, i32, C.c_int, vp, vp]),
@@ -167,6 +171,27 @@ def hop_map_mc(spec: np.ndarray, idx: np.ndarray, coef: np.ndarray):
     _check(lib().or_hop_map_mc(spec.ctypes.data, T, P, Mc, M, idx.ctypes.data, coef.ctypes.data, G, K,
                                out.ctypes.data))
     return out
+
+
+def velocity(scene, frames: np.ndarray, loc: np.ndarray, doppler_scale: float, spacing: float,
+             half: int, os_doppler: int = 1, method: str = "hop"):
+    """hop_velocity / direct_velocity at the located bins: frames complex
+    [T, P, Mc, N] -> (velocity-grid index [T], value [T])."""
+    frames = np.ascontiguousarray(frames, dtype=np.complex128)
+    T, P, Mc, N = frames.shape
+    loc = np.ascontiguousarray(loc, dtype=np.int64)
+    vidx = np.zeros(T, dtype=np.int64)
+    vval = np.zeros(T)
+    w, g = scene.c_wave(), scene.c_grid()
+    if method == "hop":
+        _check(lib().or_hop_velocity(frames.ctypes.data, T, Mc, C.byref(w), C.byref(g), doppler_scale,
+                                     spacing, half, os_doppler, loc.ctypes.data, vidx.ctypes.data,
+                                     vval.ctypes.data))
+    else:
+        _check(lib().or_direct_velocity(frames.ctypes.data, T, Mc, C.byref(w), C.byref(g),
+                                        doppler_scale, spacing, half, loc.ctypes.data,
+                                        vidx.ctypes.data, vval.ctypes.data))
+    return vidx, vval
 
 
 def direct_map(scene, frames: np.ndarray, magnitude: bool = False, threads: int | None = None):

@@ -45,6 +45,25 @@ class CudaError(RuntimeError):
 _EXC = {1: InvalidArgument, 2: GridhopRuntimeError, 3: DomainError, 4: CudaError}
 
 
+class VelocityGridC(C.Structure):
+    """gh_velocity_grid: VelocityGrid (model.hpp:93-107) + doppler_scale."""
+    _fields_ = [("doppler_scale", C.c_double), ("spacing", C.c_double), ("half", C.c_int32),
+                ("os_doppler", C.c_int32)]
+
+
+def velocity_grid(f0: float, chirp_duration: float, n_chirps: int, speed_bound: float,
+                  density: float, os_doppler: int = 1, c: float = 299792458.0) -> VelocityGridC:
+    """VelocityGrid::build (model.cpp:116-125) and doppler_scale (model.hpp:38-40)."""
+    if not (density > 0):
+        raise InvalidArgument("velocity grid: density must be positive")
+    if not (speed_bound > 0):
+        raise InvalidArgument("velocity grid: speed bound must be positive")
+    speed_res = c / (2.0 * f0 * chirp_duration * n_chirps)
+    spacing = speed_res / density
+    half = int(np.floor(speed_bound / spacing + 1e-9))
+    return VelocityGridC(f0 * chirp_duration * n_chirps / c, spacing, half, os_doppler)
+
+
 class Mrf1Header(C.Structure):
     """gh_mrf1_header: the MRF1 capture header (frame_io.hpp:10-16)."""
     _fields_ = [("n_rx", C.c_int32), ("n_chirps", C.c_int32), ("n_samples", C.c_int32),
@@ -109,6 +128,10 @@ def lib() -> C.CDLL:
             "gh_scene_hash": (u64, [i32, i32, i32, f64, f64, f64, vp, vp]),
             "gh_indirect_argmin_d": (C.c_int, [vp, P(CWave), P(CGrid), vp, i32, vp, vp, vp]),
             "gh_hop_map_mc_d": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+            "gh_hop_velocity_d": (C.c_int, [vp, P(CWave), P(CGrid), P(VelocityGridC), vp, i32, i32,
+                                            vp, vp, vp]),
+            "gh_direct_velocity_d": (C.c_int, [vp, P(CWave), P(CGrid), P(VelocityGridC), vp, i32,
+                                               i32, vp, vp, vp]),
             "gh_hop_argmax_mc_d": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
             "gh_mrf1_write": (C.c_int, [C.c_char_p, P(Mrf1Header), vp, vp]),
             "gh_mrf1_read": (C.c_int, [C.c_char_p, P(Mrf1Header), vp, i32, vp, i64]),
@@ -320,6 +343,23 @@ def hop_argmax_mc(ctx: Context, table: HopTable, frames):
     val = torch.empty(T, dtype=torch.float32, device=frames.device)
     _check(lib().gh_hop_argmax_mc_d(ctx.h, table.h, _ptr(frames), T, Mc, _ptr(idx), _ptr(val)))
     return idx, val
+
+
+def velocity(ctx: Context, scene: Scene, vgrid: VelocityGridC, frames, loc, method: str = "hop"):
+    """hop_velocity / direct_velocity (src/hopping.cpp:185-236,
+    src/direct.cpp:145-228) of multi-chirp frames [T, P, Mc, N] at the
+    located bins loc int64 [T]: (velocity-grid index [T], value [T])."""
+    torch = _torch()
+    frames = _as_float_frames_mc(frames)
+    T, P, Mc, N = frames.shape
+    loc = loc.to(device=frames.device, dtype=torch.int64).contiguous()
+    vidx = torch.empty(T, dtype=torch.int64, device=frames.device)
+    vval = torch.empty(T, dtype=torch.float32, device=frames.device)
+    w, g = scene.c_wave(), scene.c_grid()
+    fn = lib().gh_hop_velocity_d if method == "hop" else lib().gh_direct_velocity_d
+    _check(fn(ctx.h, C.byref(w), C.byref(g), C.byref(vgrid), _ptr(frames), T, Mc, _ptr(loc),
+              _ptr(vidx), _ptr(vval)))
+    return vidx, vval
 
 
 def mrf1_write(path, frames: np.ndarray, f0: float, bandwidth: float, chirp_duration: float,

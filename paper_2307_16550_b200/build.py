@@ -16,7 +16,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgridhop_b200.so"
 SOURCES = ["gh_api.cu", "gh_fft.cu", "gh_table.cu", "gh_gather.cu", "gh_direct.cu",
-           "gh_direct_umma.cu", "gh_peaks.cu", "gh_topk.cu", "gh_indirect.cu"]
+           "gh_direct_umma.cu", "gh_peaks.cu", "gh_topk.cu", "gh_indirect.cu",
+           "gh_velocity.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

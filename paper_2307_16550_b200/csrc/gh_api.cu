@@ -1181,4 +1181,46 @@ int gh_mrf1_read(const char* path, gh_mrf1_header* hdr, double* rx_xy, int32_t r
   });
 }
 
+static int velocity_entry(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                          const gh_velocity_grid* vg, const float* frames_d, int32_t n_trials,
+                          int32_t n_chirps, const int64_t* loc_d, int64_t* vidx_d, float* vval_d,
+                          bool hop) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !vg || (n_trials > 0 && (!frames_d || !loc_d || !vidx_d || !vval_d)))
+      fail(GH_EINVAL, "velocity: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    if (n_chirps < 1) fail(GH_EINVAL, "waveform: n_chirps must be >= 1");
+    if (vg->half < 0) fail(GH_EINVAL, hop ? "hop velocity: empty grid" : "velocity scan: empty grid");
+    if (hop && vg->os_doppler < 1) fail(GH_EINVAL, "hop velocity: oversampling must be >= 1");
+    if (!(std::isfinite(vg->doppler_scale) && std::isfinite(vg->spacing) && vg->spacing > 0.0))
+      fail(GH_EINVAL, "velocity grid: spacing must be positive");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx;
+    const double* tr = upload_txrx(c, wave, txrx);
+    gh::launch_velocity(c, tr, wave, grid, vg, reinterpret_cast<const float2*>(frames_d),
+                        n_trials, n_chirps, loc_d, hop, vidx_d, vval_d);
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+    txrx.release();
+  });
+}
+
+int gh_hop_velocity_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                      const gh_velocity_grid* vgrid, const float* frames_d, int32_t n_trials,
+                      int32_t n_chirps, const int64_t* loc_d, int64_t* vidx_d, float* vval_d) {
+  return velocity_entry(ctx, wave, grid, vgrid, frames_d, n_trials, n_chirps, loc_d, vidx_d,
+                        vval_d, true);
+}
+
+int gh_direct_velocity_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
+                         const gh_velocity_grid* vgrid, const float* frames_d,
+                         int32_t n_trials, int32_t n_chirps, const int64_t* loc_d,
+                         int64_t* vidx_d, float* vval_d) {
+  return velocity_entry(ctx, wave, grid, vgrid, frames_d, n_trials, n_chirps, loc_d, vidx_d,
+                        vval_d, false);
+}
+
 }  // extern "C"

@@ -233,6 +233,10 @@ void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
 void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
                  int64_t* idx_d,
                  float* val_d);
+// velocity stage (gh_velocity.cu): hop (Doppler spectrum lookups) or direct
+void launch_velocity(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
+                     const gh_velocity_grid* vg, const float2* frames_d, int T, int Mc,
+                     const int64_t* loc_d, bool hop, int64_t* vidx_d, float* vval_d);
 // indirect pipeline, location stage (gh_indirect.cu)
 void launch_range_peaks(Ctx* ctx, const float2* spec_d, int64_t rows, int M, int os,
                         double* rhat_d);
