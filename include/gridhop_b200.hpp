@@ -144,6 +144,39 @@ inline HopTable load_hop_table(Context& ctx, const std::string& path, const Scen
   return HopTable(t);
 }
 
+// Capture (frame_io.hpp:17-21) with frames flattened trial-major:
+// frames[((t * n_rx + q) * n_chirps + m) * n_samples + s]
+struct Capture {
+  gh_mrf1_header header{};
+  std::vector<double> rx;     // {x0, y0, x1, y1, ...}
+  std::vector<cplx> frames;
+};
+
+// read_frames (frame_io.hpp:27): validates like the reference, throws its
+// exception types and texts
+inline Capture read_frames(const std::string& path) {
+  Capture cap;
+  check(gh_mrf1_read(path.c_str(), &cap.header, nullptr, 0, nullptr, 0));
+  cap.rx.resize(2 * size_t(cap.header.n_rx));
+  cap.frames.resize(size_t(cap.header.n_frames) * cap.header.n_rx * cap.header.n_chirps *
+                    cap.header.n_samples);
+  check(gh_mrf1_read(path.c_str(), &cap.header, cap.rx.data(), cap.header.n_rx,
+                     reinterpret_cast<double*>(cap.frames.data()),
+                     static_cast<int64_t>(cap.frames.size())));
+  return cap;
+}
+
+// write_frames (frame_io.hpp:23-25)
+inline void write_frames(const std::string& path, const Capture& cap) {
+  if (cap.rx.size() != 2 * size_t(cap.header.n_rx))
+    throw std::invalid_argument(path + ": frame/receiver count mismatch");
+  if (cap.frames.size() != size_t(cap.header.n_frames) * cap.header.n_rx *
+                               cap.header.n_chirps * cap.header.n_samples)
+    throw std::invalid_argument(path + ": frame shape mismatch");
+  check(gh_mrf1_write(path.c_str(), &cap.header, cap.rx.data(),
+                      reinterpret_cast<const double*>(cap.frames.data())));
+}
+
 struct Estimates {
   std::vector<int64_t> bin;  // per trial, argmax_index rule (direct.cpp:55-62)
   std::vector<double> value;

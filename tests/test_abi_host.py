@@ -87,6 +87,23 @@ int main(int argc, char** argv) {
   if (back.scene_hash != h || std::memcmp(idx, idx2, sizeof idx) ||
       std::memcmp(coef, coef2, sizeof coef))
     return 2;
+  // MRF1 capture through the read_frames / write_frames wrappers
+  gb::Capture cap;
+  cap.header = gh_mrf1_header{2, 4, 8, 3, 24e9, 250e6, 128e-6, {0.5, -0.25}};
+  cap.rx = {10, 0, -3, 7};
+  for (int i = 0; i < 3 * 2 * 4 * 8; ++i) cap.frames.push_back({0.25 * i, -1.0 * i});
+  const std::string mrf = std::string(argv[1]) + ".mrf";
+  gb::write_frames(mrf, cap);
+  const gb::Capture back2 = gb::read_frames(mrf);
+  if (back2.frames != cap.frames || back2.rx != cap.rx || back2.header.n_chirps != 4) return 4;
+  try {
+    gb::Capture bad = cap;
+    bad.header.n_chirps = 1;
+    bad.frames.resize(3 * 2 * 1 * 8);
+    gb::write_frames(mrf, bad);
+    return 5;
+  } catch (const std::invalid_argument&) {
+  }
   try {
     gb::check(gh_ght1_read("/nonexistent.ght", &back, nullptr, nullptr, 0));
   } catch (const std::runtime_error& e) {
