@@ -116,6 +116,7 @@ void free_table(gh::Table* t) {
   cudaFree(t->plan.rows_d);
   cudaFree(t->plan.coef3_d);
   cudaFree(t->plan.binid_d);
+  cudaFree(t->plan.crow_d);
   delete t;
 }
 

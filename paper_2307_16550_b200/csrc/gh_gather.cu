@@ -49,6 +49,9 @@ struct GatherArgs {
   const uint16_t* rows;   // [entries][p4], 16-byte units
   const float2* coef3;    // [entries][P][3]
   const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
+  const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
+  int cbits;              // bits per ring row in crow
+  int ring;               // staged rows per pair (full-ring plan)
   gh_grid grid;
   int64_t G;              // bins of the table (shard)
   int64_t bin0;           // global index of the shard's first bin
@@ -109,7 +112,10 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
 }
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL>
+// CP (compact rows, full-ring K = 1 plans with P * bits(ring) <= 32): one
+// 32-bit word per bin holds every pair's ring row, so a step needs a single
+// shuffle instead of two
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL, bool CP = false>
 __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(GatherArgs a) {
   constexpr int kGatherThreads = gather_threads<K3, FULL>();
   constexpr int ES = K3 ? 8 : 4;         // staged element bytes
@@ -216,17 +222,25 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     nxt[q] = make_uint2(0u, 0u);
   }
   if (w0 + lane < w1) {
+    if constexpr (CP) {
+      cur[0].x = __ldg(a.crow + entry0 + w0 + lane);
+    } else {
 #pragma unroll
-    for (int q = 0; q < PQ; ++q)
-      if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
+      for (int q = 0; q < PQ; ++q)
+        if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
+    }
   }
   mbar_wait(&stage_bar, phase);
   phase ^= 1u;
   for (int64_t blk = w0; blk < w1; blk += 32) {
     if (blk + 32 + lane < w1) {
+      if constexpr (CP) {
+        nxt[0].x = __ldg(a.crow + entry0 + blk + 32 + lane);
+      } else {
 #pragma unroll
-      for (int q = 0; q < PQ; ++q)
-        if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
+        for (int q = 0; q < PQ; ++q)
+          if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
+      }
     }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
     // one step: lane group `sub` handles bin j = s * BPW + sub of the block
@@ -236,9 +250,18 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
       float2 acc[2];
       acc[0] = acc[1] = f2(0.f, 0.f);
       const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
+      if constexpr (CP) {
+        const unsigned wd = __shfl_sync(0xffffffffu, cur[0].x, j & 31);
+        const unsigned mask = (1u << a.cbits) - 1u;
+#pragma unroll
+        for (int p = 0; p < PC; ++p) {
+          const unsigned r = (wd >> (a.cbits * p)) & mask;
+          accumulate<TB, K3, MAG, L>(smv, (unsigned)(p * a.ring + r) * L, nullptr, acc, p == 0);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < PQ; ++q) {
-        if (q >= pq) break;
+        if (CP || q >= pq) break;
         const unsigned ex = __shfl_sync(0xffffffffu, cur[q].x, j & 31);
         const unsigned ey = __shfl_sync(0xffffffffu, cur[q].y, j & 31);
         const unsigned o[4] = {ex & 0xffffu, ex >> 16, ey & 0xffffu, ey >> 16};
@@ -346,10 +369,10 @@ __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* id
   val[t] = __uint_as_float((unsigned)(k >> 32));
 }
 
-template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL>
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ, bool FULL, bool CP = false>
 void run_k(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   constexpr int NT = gather_threads<K3, FULL>();
-  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ, FULL>;
+  auto kern = k_gather<TB, K3, MAG, MAPMODE, PC, PQ, FULL, CP>;
   GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   if (FULL) {
@@ -370,6 +393,12 @@ template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int PQ>
 void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
   if constexpr (TB == 16) {
     if (a.full) {  // full-ring plans are built with 16-trial batches only
+      if constexpr (!K3 && !MAPMODE && PC == 3) {
+        if (a.crow) {
+          run_k<TB, K3, MAG, MAPMODE, PC, PQ, true, true>(ctx, a, grid, smem);
+          return;
+        }
+      }
       run_k<TB, K3, MAG, MAPMODE, PC, PQ, true>(ctx, a, grid, smem);
       return;
     }
@@ -414,6 +443,9 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.rows = pl.rows_d;
   a.coef3 = pl.coef3_d;
   a.binid = pl.full ? pl.binid_d : nullptr;
+  a.crow = pl.full ? pl.crow_d : nullptr;
+  a.cbits = pl.cbits;
+  a.ring = t->M;
   a.grid = t->grid;
   a.G = t->G;
   a.bin0 = t->bin0;

@@ -145,6 +145,8 @@ struct Plan {
   uint16_t* rows_d = nullptr;    // [entries][p4] first staged row per pair
   float2* coef3_d = nullptr;     // [entries][P][3] (k3 only)
   uint32_t* binid_d = nullptr;   // [entries] global bin of each entry (permuted plans)
+  uint32_t* crow_d = nullptr;    // [entries] compact ring rows (cbits per pair), or null
+  int cbits = 0;
   int64_t n_entries = 0;
 };
 

@@ -439,6 +439,26 @@ void permute_for_banks(Ctx* ctx, Table* t) {
   GH_CUDA(cudaMalloc(&pl.binid_d, sizeof(uint32_t) * n));
   GH_CUDA(cudaMemcpyAsync(pl.binid_d, binid.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
                           ctx->stream));
+  // compact rows when every pair's ring row fits one 32-bit word (c1/c2:
+  // 3 x 10 bits): the gather then shuffles one word per step, not two
+  int bits = 1;
+  while ((1 << bits) < t->M) ++bits;
+  std::vector<uint32_t> crow;
+  if (P * bits <= 32) {
+    crow.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t w = 0;
+      for (int p = 0; p < P; ++p) {
+        const uint32_t r = prow[static_cast<size_t>(i) * p4 + p] / L - static_cast<uint32_t>(p * t->M);
+        w |= r << (bits * p);
+      }
+      crow[static_cast<size_t>(i)] = w;
+    }
+    GH_CUDA(cudaMalloc(&pl.crow_d, sizeof(uint32_t) * n));
+    GH_CUDA(cudaMemcpyAsync(pl.crow_d, crow.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    pl.cbits = bits;
+  }
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
