@@ -22,6 +22,8 @@
 // contiguous TB-run per range bin — as power, magnitude or complex.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gh_internal.cuh"
 
 namespace gh {
@@ -586,7 +588,6 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
   float4* buf = smem4;
   float2* ptw = reinterpret_cast<float2*>(smem4 + PAIRS * F::PITCH);
   float2* ltw = ptw + F::TWN;  // load twiddles W_M^{jn} at [(j-1) N + n]
-  const int tb = blockIdx.x, p = blockIdx.y;
   const double inv_n = 1.0 / (double)N;
   // pass twiddles: pass ps (stride NS, radix R) holds W_M^{r k M/(NS R)} at
   // [k][r-1]; the first pass needs none
@@ -605,14 +606,18 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
     const int j = e / N + 1, n = e % N;
     ltw[e] = __ldg(a.tw + j * n);
   }
-  // frames of the next row group are fetched into registers while the
-  // current group runs its passes (hides the HBM latency behind barriers)
+  // Persistent CTAs walk the (trial batch, pair) items; the frames of the
+  // next row group — of this item, or the first group of the CTA's next
+  // item — are fetched into registers while the current group runs its
+  // passes, so no group waits on HBM latency (not even an item's first).
+  const int n_tb = (a.T + a.tb - 1) / a.tb;
+  const int n_items = n_tb * a.P;
   constexpr int LPT = (PAIRS * N + NT - 1) / NT;
   float2 pre[SYNTH ? 1 : LPT][2];
-  const float2* frames =  // row r of the batch at + r P N
-      SYNTH ? nullptr : a.frames + ((int64_t)tb * a.tb * a.P + p) * N;
-  const int rows_left = a.T - tb * a.tb;  // rows of this batch that exist
-  auto fetch = [&](int g) {
+  auto fetch = [&](int item, int g) {
+    const int ftb = item % n_tb, fp = item / n_tb;
+    const float2* fr = a.frames + ((int64_t)ftb * a.tb * a.P + fp) * N;  // row r: + r P N
+    const int left = a.T - ftb * a.tb;
 #pragma unroll
     for (int u = 0; u < LPT; ++u) {
       const int e = threadIdx.x + u * NT;
@@ -620,14 +625,18 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
       for (int h = 0; h < 2; ++h) {
         float2 v = make_float2(0.f, 0.f);
         const int r = g + 2 * (e >> LN) + h;
-        if ((PAIRS * N % NT == 0 || e < PAIRS * N) && r < rows_left)
-          v = __ldg(frames + (int64_t)r * a.P * N + (e & (N - 1)));
+        if ((PAIRS * N % NT == 0 || e < PAIRS * N) && r < left)
+          v = __ldg(fr + (int64_t)r * a.P * N + (e & (N - 1)));
         pre[u][h] = v;
       }
     }
   };
-  if constexpr (!SYNTH) fetch(0);
+  if constexpr (!SYNTH)
+    if ((int)blockIdx.x < n_items) fetch(blockIdx.x, 0);
   __syncthreads();  // twiddle tables
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+  const int tb = item % n_tb, p = item / n_tb;
+  const int rows_left = a.T - tb * a.tb;  // rows of this batch that exist
   for (int g0 = 0; g0 < a.tb; g0 += ROWS) {
     if constexpr (SYNTH) {
       if (threadIdx.x < ROWS) {
@@ -669,8 +678,10 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
         cx_st(row + j * F::SUBP, cx_mul(y, w.x, w.y));
       }
     }
-    if constexpr (!SYNTH)
-      if (g0 + ROWS < a.tb) fetch(g0 + ROWS);
+    if constexpr (!SYNTH) {
+      if (g0 + ROWS < a.tb) fetch(item, g0 + ROWS);
+      else if (item + (int)gridDim.x < n_items) fetch(item + gridDim.x, 0);
+    }
     __syncthreads();
     fixed_passes<LN, LOS, LP, 0>(buf, ptw);
     // epilogue: output bin k = os * m + j lives in sub-row j at m
@@ -723,6 +734,7 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
     }
     __syncthreads();
   }
+  }  // items
 }
 
 int ilog2(int v) {
@@ -849,6 +861,14 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
                                static_cast<int>(smem)));
   const int n_tb = (T + tb - 1) / tb;
   dim3 grid(n_tb, P);
+  if (kern != k_fft) {
+    // fixed kernels are persistent over the (batch, pair) items
+    int occ = 0;
+    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    const int64_t items = (int64_t)n_tb * P;
+    grid = dim3(static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)std::max(occ, 1) * ctx->num_sms))));
+  }
   KTimer kt(ctx, synth ? "synth_fft" : "fft");
   kern<<<grid, threads, smem, ctx->stream>>>(a);
   GH_LAUNCHED(ctx);
