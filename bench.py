@@ -265,8 +265,9 @@ def run_ours(args, world, rank, local):
 
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    ctx.reset_timing()
-    ctx.set_timing(True)
+    # The headline loop carries only the step events: per-kernel event pairs
+    # cost ~5 % of a c2 step, so the kernel times for the roofline come from
+    # a second pass of the same K steps (same L2 flush) with them enabled.
     launches0 = ctx.launches
     barrier()
     with ClockSampler(local) as clk:
@@ -281,9 +282,16 @@ def run_ours(args, world, rank, local):
         t_wall = time.perf_counter() - t_wall
     barrier()
     launches = ctx.launches - launches0 - 0
-    ctx.set_timing(False)
     ms_steps = [a.elapsed_time(b) for a, b in evs]
     ms = sum(ms_steps) / len(ms_steps)
+    ctx.reset_timing()
+    ctx.set_timing(not args.no_kernel_timing)
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.zero_()
+            step()
+    ctx.synchronize()
+    ctx.set_timing(False)
     g_ms, g_n = ctx.kernel_time("gather")
     f_ms, f_n = ctx.kernel_time("fft")
     d_ms, d_n = ctx.kernel_time("decode")
@@ -410,6 +418,7 @@ def run_ours(args, world, rank, local):
     t_launch = T // g_launches
     g_launch_ms = g_avg / g_launches
     lsu_bytes = t_launch * G * P * (4.0 if sc.k == 1 else 24.0)
+    g_launch_ms = max(g_launch_ms, 1e-9)  # (no kernel timing: diagnostic runs only)
     achieved = lsu_bytes / (g_launch_ms * 1e-3) / 1e9
     # staged spectra (fp32 power, or complex64 for K = 3) + table rows
     hbm_bytes = (t_launch * P * sc.n_fft * (4.0 if sc.k == 1 else 8.0) + G * 8
@@ -428,6 +437,8 @@ def run_ours(args, world, rank, local):
                    "parallelism": f"trial-sharded x{world}"},
         "trials_per_s": T * world / (ms * 1e-3),
         "wall_ms_per_step": t_wall * 1e3 / args.steps,
+        "kernel_timing": "per-kernel CUDA events on the launching stream, in a second pass of "
+                         "the same steps (the headline pass has only the step events)",
         "kernels_ms": {"fft": f_ms / args.steps, "gather": g_avg, "decode": d_ms / args.steps,
                        **({"topk": k_ms / args.steps} if topk else {})},
         "launches_per_step": {"fft": f_n // args.steps, "gather": g_n // args.steps},
@@ -552,6 +563,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-direct", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
+    ap.add_argument("--no-kernel-timing", action="store_true",
+                    help="diagnostic: no per-kernel CUDA events inside the timed steps")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
