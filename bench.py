@@ -318,6 +318,17 @@ def run_ours(args, world, rank, local):
         gh.api.hop_estimate_ptr(ctx, table, fr_host.data_ptr(), T, S.POWER, idx_h.data_ptr(),
                                 val_h.data_ptr())
     e2e_s = (time.perf_counter() - t0) / args.steps
+    # this box's raw pinned H2D rate (one 123 MB-class copy), the bound e2e
+    # runs against when the frames cross PCIe as complex128
+    dst = torch.empty(fr_host.shape, dtype=fr_host.dtype, device=f"cuda:{local}")
+    dst.copy_(fr_host, non_blocking=True)
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(3):
+        dst.copy_(fr_host, non_blocking=True)
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * fr_host.numel() * fr_host.element_size() / (time.perf_counter() - h0) / 1e9
+    del dst
     if dist:
         t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -458,7 +469,9 @@ def run_ours(args, world, rank, local):
                              "peak_gbs": pk.get("hbm_gbs")}},
         "e2e": {"value": units_step / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": T * P * N * 16, "d2h_bytes_per_step": T * (8 + 4),
-                "ms_per_step": e2e_s * 1e3, "api": "gh_hop_estimate (host complex128 frames)"},
+                "ms_per_step": e2e_s * 1e3, "api": "gh_hop_estimate (host complex128 frames)",
+                "h2d_gbs_raw": h2d_gbs,
+                "h2d_bound_ms": T * P * N * 16 / (h2d_gbs * 1e9) * 1e3},
         "campaign": {"ms_per_step": camp_ms, "trials_per_s": T * world / (camp_ms * 1e-3),
                      "value": units_step / (camp_ms * 1e-3),
                      "api": "gh_campaign_hop_d (synthesis fused into the FFT)"},
