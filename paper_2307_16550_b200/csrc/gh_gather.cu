@@ -56,6 +56,8 @@ struct GatherArgs {
   int64_t G;              // bins of the table (shard)
   int64_t bin0;           // global index of the shard's first bin
   int n_batches;          // trial batches (full plan: persistent work split)
+  int n_tiles;            // tiled plan
+  int chunk_pairs;        // tiled plan: pairs per staging chunk
   int full;
   int P, p4, M, T;
   float* map;             // parity mode [T][G]
@@ -356,6 +358,233 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   }  // work items
 }
 
+// ---- tiled plans: persistent CTAs over (tile, trial batch) items, batch
+// major so the tiles of a batch run together and its spectra stay
+// L2-resident. The windows are staged in pair chunks, each with its own
+// shared-memory region and mbarrier: the last warp to finish reading chunk c
+// of an item (a shared-memory counter) restages chunk c for the CTA's next
+// item right away, so the staging of item i + 1 runs under the gather of
+// item i and no warp idles as a producer. Warps walk the pairs chunk by
+// chunk with the per-bin sums in registers (up to SMAX warp steps per pass),
+// the row words of the next step in flight while the current one
+// accumulates; the last chunk finishes each step (argmax or map store).
+// CTA warps including the producer: a multiple of 4 so the register file
+// splits evenly over the SM sub-partitions (20 warps -> 96 registers, 16 ->
+// 128); 20 measured faster than 24 (80 registers, spills) on c5
+template <bool K3>
+constexpr int tiled_warps() { return K3 ? 16 : 20; }
+template <bool K3>
+constexpr int tiled_smax() { return K3 ? 6 : 8; }
+
+// issue the bulk copies of chunk c of `item` (one thread; out of line so the
+// gather loop keeps its registers)
+template <int TB, int ES, int L, int CPP>
+__device__ __noinline__ void stage_chunk(const GatherArgs& a, int P, int64_t item, int c,
+                                         unsigned char* smraw, uint64_t* bar) {
+  const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
+  const int4* win = a.win + (int64_t)tile * a.P;
+  const uint4* spec = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(a.spec) +
+                                                     (int64_t)tb * a.P * a.M * TB * ES);
+  uint4* sm4 = reinterpret_cast<uint4*>(smraw);
+  const int p0 = c * CPP, p1 = p0 + CPP < P ? p0 + CPP : P;
+  uint32_t total = 0;
+  for (int p = p0; p < p1; ++p) total += (uint32_t)__ldg(&win[p].y) * 16u * L;
+  mbar_expect_tx(bar, total);
+  for (int p = p0; p < p1; ++p) {
+    const int4 w = __ldg(&win[p]);
+    const uint4* src = spec + (int64_t)p * a.M * L;
+    uint4* dst = sm4 + (int64_t)w.z * L;
+    for (int r = 0, gi = w.x; r < w.y; gi = 0) {  // K = 3 rings wrap twice
+      const int n = a.M - gi < w.y - r ? a.M - gi : w.y - r;
+      bulk_g2s(dst + (int64_t)r * L, src + (int64_t)gi * L, (uint32_t)n * 16u * L, bar);
+      r += n;
+    }
+  }
+  mbar_arrive(bar);
+}
+
+template <int TB, bool K3, bool MAG, bool MAPMODE, int PC, int CQ, int NWT>
+__global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
+  constexpr int NW = NWT - 1;  // consumer warps; warp NW is the producer
+  constexpr int NT = NW * 32;
+  constexpr int ES = K3 ? 8 : 4;
+  constexpr int L = TB * ES / 16;
+  constexpr int TPL = 16 / ES;
+  constexpr int BPW = 32 / L;
+  constexpr int CPP = 4 * CQ;  // pairs per chunk
+  constexpr int SMAX = tiled_smax<K3>();
+  constexpr int kMaxChunks = 16;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ float red_v[2][NW * TB];
+  __shared__ int red_i[2][NW * TB];
+  __shared__ __align__(8) uint64_t full_bar[kMaxChunks], empty_bar[kMaxChunks];
+  const int P = PC ? PC : a.P;
+  const int NC = (P + CPP - 1) / CPP;
+  const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);
+  const int64_t n_items = (int64_t)a.n_tiles * a.n_batches;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < NC; ++c) {
+      mbar_init(&full_bar[c], 1);
+      mbar_init(&empty_bar[c], NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == NW) {  // ---- producer: one lane issues the bulk copies
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it)
+        for (int c = 0; c < NC; ++c) {
+          if (it > 0) mbar_wait(&empty_bar[c], (it - 1) & 1u);
+          stage_chunk<TB, ES, L, CPP>(a, P, item, c, smraw, &full_bar[c]);
+        }
+    }
+    return;
+  }
+  // ---- consumers
+  const int sub = lane / L, v = lane % L;
+  const float4* smv = reinterpret_cast<const float4*>(smraw) + v;  // this lane's column
+  const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
+  uint32_t it = 0;
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
+    const TileDesc td = a.tiles[tile];
+    const int64_t entry0 = td.entry_off;
+    const int nb = td.wx * td.wy * td.wz;
+    const int per_warp = ((nb + NW - 1) / NW + BPW - 1) / BPW * BPW;
+    const int w0 = warp * per_warp < nb ? warp * per_warp : nb;
+    const int w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
+    const int nsteps = (w1 - w0 + BPW - 1) / BPW;
+    const int npass = nsteps > SMAX ? (nsteps + SMAX - 1) / SMAX : 1;
+    float best[TPL];
+    int blb[TPL];
+#pragma unroll
+    for (int i = 0; i < TPL; ++i) {
+      best[i] = -1.0f;
+      blb[i] = -1;
+    }
+    for (int pass = 0; pass < npass; ++pass) {
+      const int sb = w0 + pass * SMAX * BPW;  // first bin of the pass
+      float2 acc[SMAX][2];
+#pragma unroll
+      for (int s = 0; s < SMAX; ++s) acc[s][0] = acc[s][1] = f2(0.f, 0.f);
+      for (int c = 0; c < NC; ++c) {
+        mbar_wait(&full_bar[c], it & 1u);
+        auto load = [&](int s, uint2 (&w)[CQ]) {
+          int lb = sb + s * BPW + sub;
+          lb = lb < w1 ? lb : w1 - 1;
+#pragma unroll
+          for (int q = 0; q < CQ; ++q)
+            if (c * CQ + q < pq) w[q] = __ldg(rows2 + (entry0 + lb) * pq + c * CQ + q);
+        };
+        uint2 wc[CQ], wn[CQ];
+#pragma unroll
+        for (int q = 0; q < CQ; ++q) wc[q] = wn[q] = make_uint2(0u, 0u);
+        if (sb < w1) load(0, wc);
+#pragma unroll
+        for (int s = 0; s < SMAX; ++s) {
+          if (sb + s * BPW >= w1) break;  // warp-uniform
+          if (s + 1 < SMAX && sb + (s + 1) * BPW < w1) load(s + 1, wn);
+          const int lb = sb + s * BPW + sub;
+          if (lb < w1) {
+            const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
+#pragma unroll
+            for (int q = 0; q < CQ; ++q) {
+              const unsigned o[4] = {wc[q].x & 0xffffu, wc[q].x >> 16, wc[q].y & 0xffffu,
+                                     wc[q].y >> 16};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int p = c * CPP + 4 * q + u;
+                if (p >= P) break;
+                accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p, acc[s], false);
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < CQ; ++q) wc[q] = wn[q];
+        }
+        if (pass == npass - 1) {  // chunk c of this item fully read
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[c]);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < SMAX; ++s) {  // the pass's bins are complete
+        const int lb = sb + s * BPW + sub;
+        if (sb + s * BPW >= w1) break;
+        if (lb >= w1) continue;
+        float vals[TPL];
+        if constexpr (!K3) {
+          vals[0] = acc[s][0].x;
+          vals[1] = acc[s][0].y;
+          vals[2 % TPL] = acc[s][1].x;
+          vals[3 % TPL] = acc[s][1].y;
+        } else {
+          vals[0] = acc[s][0].x;
+          vals[1] = acc[s][0].y;
+        }
+        if constexpr (MAPMODE) {
+          const int64_t gb = global_bin(a, td, entry0, lb);
+#pragma unroll
+          for (int i = 0; i < TPL; ++i) {
+            const int trial = tb * TB + v * TPL + i;
+            if (trial < a.T) a.map[(int64_t)trial * a.G + (gb - a.bin0)] = vals[i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < TPL; ++i)
+            if (vals[i] > best[i]) {
+              best[i] = vals[i];
+              blb[i] = lb;
+            }
+        }
+      }
+    }
+    if constexpr (!MAPMODE) {
+      // merge the warp's lane groups, then the warps (red buffers alternate
+      // by item, so one barrier per item suffices)
+      float* rv = red_v[it & 1u];
+      int* ri = red_i[it & 1u];
+#pragma unroll
+      for (int i = 0; i < TPL; ++i) {
+        for (int o = L; o < 32; o <<= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, best[i], o);
+          const int oi = __shfl_xor_sync(0xffffffffu, blb[i], o);
+          if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && oi < blb[i]))) {
+            best[i] = ov;
+            blb[i] = oi;
+          }
+        }
+        if (sub == 0) {
+          rv[warp * TB + v * TPL + i] = best[i];
+          ri[warp * TB + v * TPL + i] = blb[i];
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      if (threadIdx.x < TB) {
+        float bv = -1.0f;
+        int bi = -1;
+        for (int w = 0; w < NW; ++w) {
+          const float val = rv[w * TB + threadIdx.x];
+          const int i = ri[w * TB + threadIdx.x];
+          if (i < 0) continue;
+          if (bi < 0 || val > bv || (val == bv && i < bi)) {
+            bv = val;
+            bi = i;
+          }
+        }
+        const int trial = tb * TB + threadIdx.x;
+        if (trial < a.T && bi >= 0) {
+          const unsigned long long gb = (unsigned long long)global_bin(a, td, entry0, bi);
+          atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                        (0xffffffffull - gb));
+        }
+      }
+    }
+  }
+}
+
 __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* idx, float* val) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
@@ -400,6 +629,26 @@ void run(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem) {
         }
       }
       run_k<TB, K3, MAG, MAPMODE, PC, PQ, true>(ctx, a, grid, smem);
+      return;
+    }
+  }
+  if constexpr (PQ == 16 && TB != 32) {
+    if (a.chunk_pairs == 16) {
+      // many pairs (17-64): the windows are staging-heavy, so the pipelined
+      // persistent kernel (measured 1.6x on BASELINE c5); with <= 16 pairs
+      // the stage-then-gather CTAs below measured as fast or faster
+      constexpr int NWT = tiled_warps<K3>();
+      auto kern = k_gather_tiled<TB, K3, MAG, MAPMODE, PC, 4, NWT>;
+      GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+      int occ = 0;
+      GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NWT * 32, smem));
+      const int64_t items = (int64_t)a.n_tiles * a.n_batches;
+      const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(
+          1, std::min<int64_t>(items, (int64_t)std::max(occ, 1) * ctx->num_sms)));
+      KTimer kt(ctx, "gather");
+      kern<<<blocks, NWT * 32, smem, ctx->stream>>>(a);
+      GH_LAUNCHED(ctx);
       return;
     }
   }
@@ -458,6 +707,8 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.keys = keys_d;
   const int n_tb = (T + pl.tb - 1) / pl.tb;
   a.n_batches = n_tb;
+  a.n_tiles = pl.n_tiles;
+  a.chunk_pairs = pl.chunk_pairs;
   if (n_tb > 65535) fail(GH_EINVAL, "gather: too many trial batches for one launch");
   const size_t smem = static_cast<size_t>(pl.max_rows) * pl.tb * pl.esize;
   // tiled plan: (tile, batch) CTAs; the full-ring plan's persistent grid is

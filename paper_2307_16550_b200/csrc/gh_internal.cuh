@@ -138,6 +138,7 @@ struct Plan {
   int esize = 4;          // staged element bytes (float power / float2 complex)
   int k3 = 0;             // 1: consecutive-triple combine with coefficients
   int p4 = 4;             // pairs padded to a multiple of 4 (row array stride)
+  int chunk_pairs = 4;    // tiled plan: pairs per staging chunk (own smem region)
   int n_tiles = 0;
   int max_rows = 0;
   TileDesc* tiles_d = nullptr;   // tiled plan

@@ -569,14 +569,21 @@ void build_plan(Ctx* ctx, Table* t) {
     GH_CUDA(cudaStreamSynchronize(ctx->stream));
   } else {
     pl.full = false;
-    // trial batch: the widest of 32 / 16 / 8 trials (power) or 16 / 8
-    // (complex) that still leaves >= 40 staged rows per pair — 128-byte rows
-    // are bank-conflict free, narrower rows trade conflicts for tile size
-    // when there are many pairs (BASELINE c5: 64)
-    pl.tb = pl.k3 ? 16 : 32;
+    // trial batch: 8 trials of power (32-byte rows) or 16 of complex
+    // spectrum (128-byte rows; 8 if that leaves < 40 staged rows per pair).
+    // Narrow power rows cost some bank conflicts but buy wider tiles, i.e.
+    // fewer staged rows per bin: measured against 16 / 32 trials on c3
+    // (15.2 vs 16.2 / 19.3 ms per 4096 trials) and c5 (2x); complex rows
+    // measured best at 16 (c4: 25.5 vs 37.9 ms at 8)
+    pl.tb = pl.k3 ? 16 : 8;
     while (pl.tb > 8 &&
            static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize)) / P < 40)
       pl.tb >>= 1;
+    // pair chunks with their own shared-memory regions for the pipelined
+    // gather (17-64 pairs: 16 pairs = 4 row-table words per chunk); one
+    // chunk otherwise
+    pl.chunk_pairs = pl.p4 > 16 ? 16 : pl.p4;
+    const int n_chunks = (P + pl.chunk_pairs - 1) / pl.chunk_pairs;
     const int budget_rows = static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize));
     const int allow = budget_rows / P - 5;
     if (allow < 4) fail(GH_EINVAL, "gather plan: too many pairs for one shared-memory window");
@@ -643,6 +650,10 @@ void build_plan(Ctx* ctx, Table* t) {
                               ctx->stream));
       GH_CUDA(cudaStreamSynchronize(ctx->stream));
       tl.win.assign(mm.size(), make_int4(0, 0, 0, 0));
+      // pair chunks own fixed shared-memory regions (the largest chunk
+      // window over all tiles), so the gather can restage chunk c of its
+      // next item while it still reads the other chunks of this one
+      std::vector<int> region(static_cast<size_t>(n_chunks), 0);
       for (size_t ti = 0; ti < nt; ++ti) {
         int rs = 0;
         for (int p = 0; p < P; ++p) {
@@ -653,11 +664,27 @@ void build_plan(Ctx* ctx, Table* t) {
             len = ring;
           }
           base = ((base % M) + M) % M;
-          tl.win[ti * P + p] = make_int4(base, len, rs, 0);
+          tl.win[ti * P + p] = make_int4(base, len, 0, 0);
           rs += len;
+          if (p % pl.chunk_pairs == pl.chunk_pairs - 1 || p == P - 1) {
+            int& r = region[static_cast<size_t>(p / pl.chunk_pairs)];
+            r = std::max(r, rs);
+            rs = 0;
+          }
+        }
+      }
+      std::vector<int> region_off(static_cast<size_t>(n_chunks), 0);
+      for (int c = 1; c < n_chunks; ++c)
+        region_off[static_cast<size_t>(c)] = region_off[c - 1] + region[c - 1];
+      tl.max_rows = region_off.back() + region.back();
+      for (size_t ti = 0; ti < nt; ++ti) {
+        int rs = 0;
+        for (int p = 0; p < P; ++p) {
+          if (p % pl.chunk_pairs == 0) rs = region_off[static_cast<size_t>(p / pl.chunk_pairs)];
+          tl.win[ti * P + p].z = rs;
+          rs += tl.win[ti * P + p].y;
         }
         tl.tiles[ti].rows = rs;
-        tl.max_rows = std::max(tl.max_rows, rs);
       }
       return tl;
     };

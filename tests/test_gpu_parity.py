@@ -332,6 +332,32 @@ def test_campaign_statistics_match_oracle(ctx):
         assert np.allclose(so, sg), (snr, so, sg)
 
 
+@pytest.mark.parametrize("P,scheme,combine,T", [
+    (64, S.NEAREST, S.POWER, 1500),  # compile-time 64 pairs, many items per CTA
+    (20, S.POLY3, S.MAGNITUDE, 700),  # runtime pair count, a partial last chunk
+    (40, S.NEAREST, S.MAGNITUDE, 333),
+])
+def test_pipelined_tiled_gather(ctx, P, scheme, combine, T):
+    # > 16 pairs: the persistent gather whose producer warp restages pair
+    # chunks of the next (tile, batch) item under the current one; enough
+    # trials that every CTA runs several items (phase flips, ring reuse)
+    sc = S.small(P=P, N=512, os=4, nx=40, ny=36, scheme=scheme)
+    fr, _ = O.synth(sc, 0, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc, magnitude=combine == S.MAGNITUDE)
+    t = gh.precompute_hop_table(ctx, sc)
+    fd = frames_to_dev(fr)
+    idx, val = gh.hop_argmax(ctx, t, fd, combine)
+    assert_argmax_parity(ref, idx.cpu().numpy(), f"P={P}")
+    iv = idx.cpu().numpy()
+    assert np.allclose(val.cpu().numpy(), ref[np.arange(T), iv], rtol=1e-4)
+    m = gh.hop_decision_map(ctx, t, fd[:97], combine).cpu().numpy()
+    assert rel_map_err(m, ref[:97]) < MAP_TOL
+    # repeated launches agree bit for bit (no stale chunk is ever read)
+    idx2, val2 = gh.hop_argmax(ctx, t, fd, combine)
+    assert torch.equal(idx, idx2) and torch.equal(val, val2)
+
+
 def c5_reduced():
     # BASELINE c5 stations/waveform (64 pairs, N = 512, os = 4, 3-D grid
     # spacing 0.195 x 0.195 x 0.3125 m) on a 48 x 40 x 8 block of the grid
