@@ -25,9 +25,12 @@
 #include <algorithm>
 
 #include "gh_internal.cuh"
+#include "gh_ptx.cuh"
 
 namespace gh {
 namespace {
+
+using namespace ptx;
 
 constexpr int kFftThreads = 512;
 constexpr int kMaxTargets = 8;
@@ -737,6 +740,198 @@ __global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs 
   }  // items
 }
 
+// ------------------------------------------- N = 256 warp-resident FFT
+// The c1/c2 size (N = 256, os = 4, M = 1024) as two register radix-16
+// stages with ONE warp-private shared-memory exchange. With n = 16 a + t
+// (a, t < 16) and k = 64 k3 + k2:
+//   stage 1  Y_t[4 k1 + j] = sum_a (y[16a+t] W_64^{a j}) W_16^{a k1}
+//   stage 2  X[64 k3 + k2] = sum_t (Y_t[k2] W_M^{t k2}) W_16^{t k3}
+// One row per lane with the complex value packed (re, im) in one fp32x2
+// register pair: a complex add is one FADD2 and a twiddle product one
+// FMUL2 + one FFMA2 on the swapped pair (sm_100 operand swizzle), so a lane
+// holds 16 points in 32 registers and an SM keeps 32 warps resident.
+// A CTA (8 warps) walks 4-trial groups of one (batch, pair); warp w owns
+// sub-FFT index j = w % 4 of rows 2 (w / 4) + h (h = lane / 16). Lane (t, h)
+// runs stage 1 on its 16 stride-16 samples; the exchange hands lane (k1, h)
+// the 16 Y_t[4 k1 + j]; stage 2 yields 16 output bins, whose power goes to
+// a CTA buffer [k][4 trials] (16-byte chunks XOR-swizzled so the scattered
+// 4-byte writes are 2-way at worst); after one barrier every bin leaves as
+// one 16-byte store into the gather layout [batch][pair][k][TB]. The
+// group's four 2 KB rows arrive by TMA bulk copies into a 2-deep ring (one
+// mbarrier per stage): the last warp to read a stage (a shared-memory
+// counter) issues the copies of the CTA's group 2 ahead into it, so no warp
+// waits as a producer.
+// Shared-memory traffic per row: 2 KB input read + one 2 KB exchange each
+// way (the Stockham kernel above moves ~28 KB per row).
+constexpr int kR16Warps = 8;
+constexpr int kR16Xp = 16 * 17;  // float2 per exchange row: [k1][t], pitch 17
+constexpr int kR16St = 2;        // input ring stages
+constexpr size_t kR16Smem =
+    (kR16St * 4 * 256 + kR16Warps * 2 * kR16Xp + 1024 * 2) * sizeof(float2);
+__constant__ float2 c_w64[64] = {
+    {1.0000000000f, -0.0000000000f}, {0.9951847267f, -0.0980171403f}, {0.9807852804f, -0.1950903220f}, {0.9569403357f, -0.2902846773f},
+    {0.9238795325f, -0.3826834324f}, {0.8819212643f, -0.4713967368f}, {0.8314696123f, -0.5555702330f}, {0.7730104534f, -0.6343932842f},
+    {0.7071067812f, -0.7071067812f}, {0.6343932842f, -0.7730104534f}, {0.5555702330f, -0.8314696123f}, {0.4713967368f, -0.8819212643f},
+    {0.3826834324f, -0.9238795325f}, {0.2902846773f, -0.9569403357f}, {0.1950903220f, -0.9807852804f}, {0.0980171403f, -0.9951847267f},
+    {0.0000000000f, -1.0000000000f}, {-0.0980171403f, -0.9951847267f}, {-0.1950903220f, -0.9807852804f}, {-0.2902846773f, -0.9569403357f},
+    {-0.3826834324f, -0.9238795325f}, {-0.4713967368f, -0.8819212643f}, {-0.5555702330f, -0.8314696123f}, {-0.6343932842f, -0.7730104534f},
+    {-0.7071067812f, -0.7071067812f}, {-0.7730104534f, -0.6343932842f}, {-0.8314696123f, -0.5555702330f}, {-0.8819212643f, -0.4713967368f},
+    {-0.9238795325f, -0.3826834324f}, {-0.9569403357f, -0.2902846773f}, {-0.9807852804f, -0.1950903220f}, {-0.9951847267f, -0.0980171403f},
+    {-1.0000000000f, -0.0000000000f}, {-0.9951847267f, 0.0980171403f}, {-0.9807852804f, 0.1950903220f}, {-0.9569403357f, 0.2902846773f},
+    {-0.9238795325f, 0.3826834324f}, {-0.8819212643f, 0.4713967368f}, {-0.8314696123f, 0.5555702330f}, {-0.7730104534f, 0.6343932842f},
+    {-0.7071067812f, 0.7071067812f}, {-0.6343932842f, 0.7730104534f}, {-0.5555702330f, 0.8314696123f}, {-0.4713967368f, 0.8819212643f},
+    {-0.3826834324f, 0.9238795325f}, {-0.2902846773f, 0.9569403357f}, {-0.1950903220f, 0.9807852804f}, {-0.0980171403f, 0.9951847267f},
+    {-0.0000000000f, 1.0000000000f}, {0.0980171403f, 0.9951847267f}, {0.1950903220f, 0.9807852804f}, {0.2902846773f, 0.9569403357f},
+    {0.3826834324f, 0.9238795325f}, {0.4713967368f, 0.8819212643f}, {0.5555702330f, 0.8314696123f}, {0.6343932842f, 0.7730104534f},
+    {0.7071067812f, 0.7071067812f}, {0.7730104534f, 0.6343932842f}, {0.8314696123f, 0.5555702330f}, {0.8819212643f, 0.4713967368f},
+    {0.9238795325f, 0.3826834324f}, {0.9569403357f, 0.2902846773f}, {0.9807852804f, 0.1950903220f}, {0.9951847267f, 0.0980171403f}};  // W_64^e
+
+__device__ __forceinline__ float2 c1_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 c1_sub(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 c1_mul(float2 x, float2 w) {  // x * w
+  return __ffma2_rn(make_float2(x.y, x.x), make_float2(-w.y, w.y),
+                    __fmul2_rn(x, make_float2(w.x, w.x)));
+}
+__device__ __forceinline__ float2 c1_mi(float2 x) { return make_float2(x.y, -x.x); }  // x * -i
+__device__ __forceinline__ float2 c1_w16(float2 x, int e) {  // x * W16^e, e constant
+  e &= 15;
+  if (e == 0) return x;
+  if (e == 4) return c1_mi(x);
+  if (e == 8) return make_float2(-x.x, -x.y);
+  if (e == 12) return make_float2(-x.y, x.x);
+  return c1_mul(x, make_float2(kC16[e], -kS16[e]));
+}
+__device__ __forceinline__ void c1_dft4(float2& a, float2& b, float2& c, float2& d) {
+  const float2 t0 = c1_add(a, c), t1 = c1_sub(a, c);
+  const float2 t2 = c1_add(b, d), t3 = c1_mi(c1_sub(b, d));
+  a = c1_add(t0, t2);
+  c = c1_sub(t0, t2);
+  b = c1_add(t1, t3);
+  d = c1_sub(t1, t3);
+}
+// forward 16-point DFT, natural order in and out (4 x 4)
+__device__ __forceinline__ void c1_dft16(float2* v) {
+  float2 y[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    float2 a = v[n2], b = v[4 + n2], c = v[8 + n2], d = v[12 + n2];
+    c1_dft4(a, b, c, d);
+    y[0 * 4 + n2] = a;
+    y[1 * 4 + n2] = c1_w16(b, n2 * 1);
+    y[2 * 4 + n2] = c1_w16(c, n2 * 2);
+    y[3 * 4 + n2] = c1_w16(d, n2 * 3);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    float2 a = y[k1 * 4 + 0], b = y[k1 * 4 + 1], c = y[k1 * 4 + 2], d = y[k1 * 4 + 3];
+    c1_dft4(a, b, c, d);
+    v[k1] = a;
+    v[k1 + 4] = b;
+    v[k1 + 8] = c;
+    v[k1 + 12] = d;
+  }
+}
+
+template <bool MAG>
+__global__ void __launch_bounds__(kR16Warps * 32, 3) k_fft256(FftArgs a) {
+  constexpr int N = 256, M = 1024, K2 = 64;
+  extern __shared__ __align__(16) float2 r16[];
+  float2* in = r16;                     // [stages][4 rows][256]
+  float2* xs = r16 + kR16St * 4 * 256;  // per warp: [h][k1][17]
+  float* ob = reinterpret_cast<float*>(xs + kR16Warps * 2 * kR16Xp);  // [k (swizzled)][4]
+  __shared__ __align__(8) uint64_t full[kR16St];
+  __shared__ int readers[kR16St];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane & 15, h = lane >> 4, j = warp & 3, row = 2 * (warp >> 2) + h;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kR16St; ++s) {
+      mbar_init(&full[s], 1);
+      readers[s] = 0;
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  float2* xw = xs + (warp * 2 + h) * kR16Xp;
+  // stage-2 twiddles W_M^{t (4 k1 + j)}: per-lane recurrences (step W_M^{4t})
+  // re-seeded exactly at k1 = 0 and 8
+  const float2 seed0 = __ldg(a.tw + t * j), seed8 = __ldg(a.tw + t * (32 + j));
+  const float2 step = __ldg(a.tw + 4 * t);
+  const int groups = a.tb >> 2;  // 4-trial groups per batch
+  const int n_tb = (a.T + a.tb - 1) / a.tb;
+  const int n_items = n_tb * a.P * groups;
+  // group g of (batch, pair): rows tb*TB + 4 g + r; rows past T repeat the
+  // last trial (finite values; the gather ignores trials >= T)
+  auto issue = [&](int item, int s) {
+    const int g = item % groups, p = (item / groups) % a.P, tb = item / (groups * a.P);
+    mbar_expect_tx(&full[s], 4u * N * sizeof(float2));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int tr = min(tb * a.tb + 4 * g + r, a.T - 1);
+      bulk_g2s(in + (s * 4 + r) * N, a.frames + ((int64_t)tr * a.P + p) * N,
+               N * sizeof(float2), &full[s]);
+    }
+    mbar_arrive(&full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kR16St; ++s)
+      if ((int)blockIdx.x + s * (int)gridDim.x < n_items) issue(blockIdx.x + s * gridDim.x, s);
+  int it = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+    const int s = it % kR16St;
+    const int g = item % groups, p = (item / groups) % a.P, tb = item / (groups * a.P);
+    mbar_wait(&full[s], (it / kR16St) & 1);
+    const float2* src = in + (s * 4 + row) * N + t;
+    float2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = src[16 * q];
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&readers[s], 1) == kR16Warps - 1) {  // last reader refills
+        readers[s] = 0;
+        const int nx = item + kR16St * (int)gridDim.x;
+        if (nx < n_items) issue(nx, s);
+      }
+    }
+    if (j != 0) {
+#pragma unroll
+      for (int q = 1; q < 16; ++q) v[q] = c1_mul(v[q], c_w64[(q * j) & 63]);
+    }
+    c1_dft16(v);
+    float2 w = seed0;
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) {
+      if (k1 == 8) w = seed8;
+      xw[k1 * 17 + t] = c1_mul(v[k1], w);
+      if (k1 != 7 && k1 != 15) w = c1_mul(w, step);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = xw[t * 17 + q];  // lane t = k1
+    __syncwarp();  // the next group overwrites the exchange rows
+    c1_dft16(v);
+    // v[k3] = X[64 k3 + 4 t + j] of row 2 (warp / 4) + h of the group
+#pragma unroll
+    for (int k3 = 0; k3 < 16; ++k3) {
+      const float2 sq = __fmul2_rn(v[k3], v[k3]);
+      const float pw = sq.x + sq.y;
+      const int k = 64 * k3 + 4 * t + j;
+      ob[4 * (k ^ ((k >> 3) & 7)) + row] = MAG ? sqrtf(pw) : pw;
+    }
+    __syncthreads();
+    float* dst = static_cast<float*>(a.out) + ((int64_t)tb * a.P + p) * M * a.tb + g * 4;
+#pragma unroll
+    for (int i = 0; i < M / (kR16Warps * 32); ++i) {
+      const int k = threadIdx.x + i * kR16Warps * 32;
+      *reinterpret_cast<float4*>(dst + (int64_t)k * a.tb) =
+          *reinterpret_cast<const float4*>(ob + 4 * (k ^ ((k >> 3) & 7)));
+    }
+    __syncthreads();  // the next group overwrites ob
+  }
+}
+
 int ilog2(int v) {
   int l = 0;
   while ((1 << l) < v) ++l;
@@ -780,9 +975,11 @@ FftKernel fixed_kernel(int ln, int los, int lp, bool synth, int out_kind, size_t
 
 const float2* twiddles(Ctx* ctx, int M) {
   if (ctx->twiddle_m != M) {
-    std::vector<float2> h(static_cast<size_t>(M));
-    for (int k = 0; k < M; ++k) {
-      const double a = -2.0 * 3.141592653589793238462643383279502884 * k / M;
+    // [0, M): W_M^k; [M, 2M): W_M^{t k2} at [k2][t], t < 16 (k_fft256)
+    std::vector<float2> h(2 * static_cast<size_t>(M));
+    for (int k = 0; k < 2 * M; ++k) {
+      const int e = k < M ? k : ((k - M) & 15) * ((k - M) >> 4) % M;
+      const double a = -2.0 * 3.141592653589793238462643383279502884 * e / M;
       h[static_cast<size_t>(k)] = make_float2((float)cos(a), (float)sin(a));
     }
     void* d = ctx->twiddle_buf.get(sizeof(float2) * h.size());
@@ -845,6 +1042,21 @@ void launch_fft(Ctx* ctx, const float2* frames_d, const SynthParams* synth, int 
   if (tb >= 2) {
     lp = ilog2(tb) - 1;
     while (lp > 0 && ((M << lp) > 4096 || lp > 3)) --lp;
+  }
+  if (!synth && N == 256 && os == 4 && tb % 4 == 0 &&
+      (out_kind == FFT_GATHER_POWER || out_kind == FFT_GATHER_MAG)) {
+    FftKernel k = out_kind == FFT_GATHER_MAG ? k_fft256<true> : k_fft256<false>;
+    GH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kR16Smem)));
+    int occ = 0;
+    GH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kR16Warps * 32, kR16Smem));
+    const int64_t items = (int64_t)((T + tb - 1) / tb) * P * (tb / 4);
+    const int64_t blocks =
+        std::min<int64_t>(items, (int64_t)std::max(occ, 1) * ctx->num_sms);
+    KTimer kt(ctx, "fft");
+    k<<<static_cast<unsigned>(blocks), kR16Warps * 32, kR16Smem, ctx->stream>>>(a);
+    GH_LAUNCHED(ctx);
+    return;
   }
   size_t fsmem = 0;
   int fthreads = 0;

@@ -114,6 +114,26 @@ def test_hop_map_and_argmax(ctx, scheme, combine):
     assert np.allclose(val.cpu().numpy(), ref[np.arange(T), iv], rtol=1e-4)
 
 
+@pytest.mark.parametrize("os_", [4, 2])
+@pytest.mark.parametrize("combine", [S.POWER, S.MAGNITUDE])
+def test_hop_c1_scene_n256(ctx, os_, combine):
+    # the c1/c2 scene (N = 256): the warp-resident two-stage FFT (k_fft256)
+    # feeding the full-ring gather; T not a multiple of the 4-trial group
+    sc = S.baseline("c1")
+    if os_ != sc.os_range:
+        sc = S.small(P=3, N=256, os=os_, nx=40, ny=30, scheme=S.NEAREST)
+    T = 45
+    fr, _ = O.synth(sc, 7, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc, magnitude=combine == S.MAGNITUDE)
+    t = gh.precompute_hop_table(ctx, sc)
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, t, fd, combine).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    idx, _ = gh.hop_argmax(ctx, t, fd, combine)
+    assert_argmax_parity(ref, idx.cpu().numpy(), f"c1 scene os={os_}")
+
+
 def test_hop_tiled_plan_k1(ctx):
     # a scene whose full ring does not fit shared memory -> tiled plan
     sc = S.small(P=12, N=512, os=4, nx=60, ny=50, scheme=S.NEAREST)
