@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   constexpr int TPL = 16 / ES;           // trials per lane
   constexpr int BPW = 32 / L;            // bins per warp step
   constexpr int NW = kGatherThreads / 32;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ float red_v[NW * TB];
   __shared__ int red_i[NW * TB];
 
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
   constexpr int CPP = 4 * CQ;  // pairs per chunk
   constexpr int SMAX = tiled_smax<K3>();
   constexpr int kMaxChunks = 16;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ float red_v[2][NW * TB];
   __shared__ int red_i[2][NW * TB];
   __shared__ __align__(8) uint64_t full_bar[kMaxChunks], empty_bar[kMaxChunks];
