@@ -50,7 +50,7 @@ def peaks() -> dict:
 # gather instantiation per BASELINE config: its ncu --set full capture in
 # profiles/ supplies roofline.traffic (DRAM read + write per launch)
 GATHER_KERNEL = {"c1": "k_gather<16, 0, 0, 0, 3, 1", "c2": "k_gather<16, 0, 0, 0, 3, 1",
-                 "c3": "k_gather<32, 0, 0, 0, 16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
+                 "c3": "k_gather<8, 0, 0, 1, 16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
 
 
 def ncu_traffic(config: str, trials: int):
@@ -74,7 +74,7 @@ def ncu_traffic(config: str, trials: int):
 
 
 # trials per launch of each committed capture (tools/evidence.sh)
-PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3g.ncu-rep": 4096, "prof_tk2.ncu-rep": 512,
+PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3_r1.ncu-rep": 2048,
                   "prof_direct_r1.ncu-rep": 1024}
 
 
