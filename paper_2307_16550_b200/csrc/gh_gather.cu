@@ -46,7 +46,8 @@ struct GatherArgs {
   const void* spec;       // [batches][P][M][TB] float or float2
   const TileDesc* tiles;  // tiled plan
   const int4* win;        // [tiles][P] / [P]
-  const uint16_t* rows;   // [entries][p4], 16-byte units
+  const uint16_t* rows;   // [p4 / 4][entries][4], 16-byte units (word-major)
+  int64_t n_entries;      // entries of the plan (word stride of rows)
   const float2* coef3;    // [entries][P][3]
   const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
   const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     } else {
 #pragma unroll
       for (int q = 0; q < PQ; ++q)
-        if (q < pq) cur[q] = __ldg(rows2 + (entry0 + w0 + lane) * pq + q);
+        if (q < pq) cur[q] = __ldg(rows2 + q * a.n_entries + entry0 + w0 + lane);
     }
   }
   mbar_wait(&stage_bar, phase);
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
       } else {
 #pragma unroll
         for (int q = 0; q < PQ; ++q)
-          if (q < pq) nxt[q] = __ldg(rows2 + (entry0 + blk + 32 + lane) * pq + q);
+          if (q < pq) nxt[q] = __ldg(rows2 + q * a.n_entries + entry0 + blk + 32 + lane);
       }
     }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
@@ -476,7 +477,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
           lb = lb < w1 ? lb : w1 - 1;
 #pragma unroll
           for (int q = 0; q < CQ; ++q)
-            if (c * CQ + q < pq) w[q] = __ldg(rows2 + (entry0 + lb) * pq + c * CQ + q);
+            if (c * CQ + q < pq)
+              w[q] = __ldg(rows2 + (int64_t)(c * CQ + q) * a.n_entries + entry0 + lb);
         };
         uint2 wc[CQ], wn[CQ];
 #pragma unroll
@@ -690,6 +692,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.tiles = pl.tiles_d;
   a.win = pl.win_d;
   a.rows = pl.rows_d;
+  a.n_entries = pl.n_entries;
   a.coef3 = pl.coef3_d;
   a.binid = pl.full ? pl.binid_d : nullptr;
   a.crow = pl.full ? pl.crow_d : nullptr;

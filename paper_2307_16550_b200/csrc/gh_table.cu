@@ -306,6 +306,7 @@ struct FillArgs {
   const double2* coef;
   int P, K, M, p4, k3, lanes;
   int64_t G, bin0;        // local bins; tiles carry global coordinates
+  int64_t n_entries;      // plan entries: row words are stored [p / 4][entry]
   uint16_t* rows;
   float2* coef3;
   int* err;
@@ -342,7 +343,9 @@ __global__ void k_fill_plan(FillArgs a) {
     // gather forms the shared-memory address with one shift-add
     const int off16 = (w.z + local) * a.lanes;
     if (off16 > 65535) atomicOr(a.err, 2);
-    a.rows[(entry0 + lb) * a.p4 + p] = (uint16_t)off16;
+    // word-major ([pair / 4][entry] of 4 x uint16): the gather's lanes load
+    // one word of consecutive entries, i.e. contiguous 8-byte runs
+    a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb) * 4 + (p & 3)] = (uint16_t)off16;
     if (a.k3) {
       float2* c3 = a.coef3 + ((entry0 + lb) * a.P + p) * 3;
       for (int j = 0; j < 3; ++j) {
@@ -368,10 +371,16 @@ void permute_for_banks(Ctx* ctx, Table* t) {
   Plan& pl = t->plan;
   const int P = t->P, p4 = pl.p4, L = pl.tb * pl.esize / 16;
   const int64_t n = pl.n_entries;
-  std::vector<uint16_t> rows(static_cast<size_t>(n) * p4);
-  GH_CUDA(cudaMemcpyAsync(rows.data(), pl.rows_d, sizeof(uint16_t) * rows.size(),
+  std::vector<uint16_t> rows(static_cast<size_t>(n) * p4), wm(rows.size());
+  GH_CUDA(cudaMemcpyAsync(wm.data(), pl.rows_d, sizeof(uint16_t) * wm.size(),
                           cudaMemcpyDeviceToHost, ctx->stream));
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  // device layout is word-major [p / 4][entry][p % 4]; work entry-major here
+  auto wm_at = [n](int64_t e, int p) {
+    return static_cast<size_t>((((int64_t)(p >> 2)) * n + e) * 4 + (p & 3));
+  };
+  for (int64_t e = 0; e < n; ++e)
+    for (int p = 0; p < p4; ++p) rows[static_cast<size_t>(e) * p4 + p] = wm[wm_at(e, p)];
   const unsigned full = (1u << P) - 1u;
   // Bins whose rows equal an earlier bin's for every pair always tie with
   // it and can never win the argmax: they go last (ascending), so entry
@@ -434,8 +443,11 @@ void permute_for_banks(Ctx* ctx, Table* t) {
                 sizeof(uint16_t) * p4);
     binid[static_cast<size_t>(i)] = static_cast<uint32_t>(t->bin0 + e);
   }
-  GH_CUDA(cudaMemcpyAsync(pl.rows_d, prow.data(), sizeof(uint16_t) * prow.size(),
+  for (int64_t e = 0; e < n; ++e)
+    for (int p = 0; p < p4; ++p) wm[wm_at(e, p)] = prow[static_cast<size_t>(e) * p4 + p];
+  GH_CUDA(cudaMemcpyAsync(pl.rows_d, wm.data(), sizeof(uint16_t) * wm.size(),
                           cudaMemcpyHostToDevice, ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));  // wm is a host temporary
   GH_CUDA(cudaMalloc(&pl.binid_d, sizeof(uint32_t) * n));
   GH_CUDA(cudaMemcpyAsync(pl.binid_d, binid.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
                           ctx->stream));
@@ -739,6 +751,7 @@ void build_plan(Ctx* ctx, Table* t) {
   f.G = t->G;
   f.bin0 = t->bin0;
   f.rows = pl.rows_d;
+  f.n_entries = pl.n_entries;
   f.coef3 = pl.coef3_d;
   f.err = err_d;
   if (pl.full) {
