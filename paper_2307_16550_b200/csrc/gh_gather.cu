@@ -48,7 +48,7 @@ struct GatherArgs {
   const int4* win;        // [tiles][P] / [P]
   const uint16_t* rows;   // [p4 / 4][entries][4], 16-byte units (word-major)
   int64_t n_entries;      // entries of the plan (word stride of rows)
-  const float2* coef3;    // [entries][P][3]
+  const float2* coef3;    // [P][3][entries] (word-major)
   const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
   const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
   int cbits;              // bits per ring row in crow
@@ -78,7 +78,7 @@ __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y
 template <int TB, bool K3, bool MAG, int L>
 __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsigned off16,
                                            const float2* __restrict__ cf, float2 (&acc)[2],
-                                           bool first) {
+                                           bool first, int64_t cs = 0) {
   if constexpr (!K3) {
     const float4 z = smv[off16];
     if (first) {
@@ -89,7 +89,7 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
       acc[1] = __fadd2_rn(acc[1], f2(z.z, z.w));
     }
   } else {
-    const float2 c0 = __ldg(cf), c1 = __ldg(cf + 1), c2 = __ldg(cf + 2);
+    const float2 c0 = __ldg(cf), c1 = __ldg(cf + cs), c2 = __ldg(cf + 2 * cs);
     const float4 z0 = smv[off16];
     const float4 z1 = smv[off16 + L];
     const float4 z2 = smv[off16 + 2 * L];
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
       const int64_t lb = blk + (!check || j < nblk ? j : 0);
       float2 acc[2];
       acc[0] = acc[1] = f2(0.f, 0.f);
-      const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
+      const float2* cf = K3 ? a.coef3 + entry0 + lb : nullptr;
       if constexpr (CP) {
         const unsigned wd = __shfl_sync(0xffffffffu, cur[0].x, j & 31);
         const unsigned mask = (1u << a.cbits) - 1u;
@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
         for (int u = 0; u < 4; ++u) {
           const int p = 4 * q + u;
           if (PC ? p >= PC : p >= a.P) break;
-          accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p, acc, p == 0);
+          accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p * a.n_entries, acc, p == 0,
+                                     a.n_entries);
         }
       }
       float vals[TPL];
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
           if (s + 1 < SMAX && sb + (s + 1) * BPW < w1) load(s + 1, wn);
           const int lb = sb + s * BPW + sub;
           if (lb < w1) {
-            const float2* cf = K3 ? a.coef3 + (entry0 + lb) * P * 3 : nullptr;
+            const float2* cf = K3 ? a.coef3 + entry0 + lb : nullptr;
 #pragma unroll
             for (int q = 0; q < CQ; ++q) {
               const unsigned o[4] = {wc[q].x & 0xffffu, wc[q].x >> 16, wc[q].y & 0xffffu,
@@ -499,7 +500,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
               for (int u = 0; u < 4; ++u) {
                 const int p = c * CPP + 4 * q + u;
                 if (p >= P) break;
-                accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p, acc[s], false);
+                accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p * a.n_entries, acc[s], false,
+                                           a.n_entries);
               }
             }
           }

@@ -347,10 +347,11 @@ __global__ void k_fill_plan(FillArgs a) {
     // one word of consecutive entries, i.e. contiguous 8-byte runs
     a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb) * 4 + (p & 3)] = (uint16_t)off16;
     if (a.k3) {
-      float2* c3 = a.coef3 + ((entry0 + lb) * a.P + p) * 3;
+      // word-major like the rows: [pair][j][entry]
       for (int j = 0; j < 3; ++j) {
         const double2 c = j < a.K ? a.coef[at + j] : make_double2(0.0, 0.0);
-        c3[j] = make_float2((float)c.x, (float)c.y);
+        a.coef3[((int64_t)p * 3 + j) * a.n_entries + entry0 + lb] =
+            make_float2((float)c.x, (float)c.y);
       }
     }
   }
