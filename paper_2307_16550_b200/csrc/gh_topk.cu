@@ -29,6 +29,7 @@ namespace {
 constexpr int kTopkThreads = 512;
 constexpr int kMaxK = 8;
 constexpr int kVec = 4;  // float4 loads in flight per thread and iteration
+constexpr int kQueue = 160;
 
 // order-preserving float -> uint32 (larger float -> larger uint)
 __device__ __forceinline__ uint32_t ord(float v) {
@@ -91,10 +92,12 @@ __device__ __forceinline__ void warp_flush(WarpTopK& w, unsigned long long* q,
   unsigned ok = __ballot_sync(0xffffffffu, cand && is_local_max(m, ck, nx, ny, nz));
   // keep the overflow (at most 31) queued
   const int rest = w.qn - n;
-  const unsigned long long moved = lane < rest ? q[32 + lane] : 0ull;
-  __syncwarp();
-  if (lane < rest) q[lane] = moved;
-  __syncwarp();
+  for (int b = 0; b < rest; b += 32) {  // shift the overflow down by 32
+    const unsigned long long moved = b + lane < rest ? q[32 + b + lane] : 0ull;
+    __syncwarp();
+    if (b + lane < rest) q[b + lane] = moved;
+    __syncwarp();
+  }
   w.qn = rest;
   while (ok) {
     const int src = __ffs(ok) - 1;
@@ -129,7 +132,6 @@ __device__ __forceinline__ void warp_offer(WarpTopK& w, unsigned long long* q,
   if (!pend) return;
   if (key > w.thr) q[w.qn + __popc(pend & ((1u << lane) - 1u))] = key;
   w.qn += __popc(pend);
-  if (w.qn >= 32) warp_flush(w, q, m, K, nx, ny, nz, cta_thr);
 }
 
 __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __restrict__ map,
@@ -140,7 +142,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
   __shared__ unsigned long long cta_thr;
   __shared__ unsigned long long lists[NW][kMaxK];
   __shared__ int counts[NW];
-  __shared__ unsigned long long queue[NW][64];  // per-warp candidates awaiting the test
+  // per-warp candidates awaiting the test: up to 31 + 4 offers of 32 between
+  // flushes (one flush site per float4 keeps the unrolled loop small enough
+  // for the instruction cache)
+  __shared__ unsigned long long queue[NW][kQueue];
   const int trial = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* m = map + (int64_t)trial * G;
@@ -156,6 +161,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
     const int64_t i = b + threadIdx.x;
     const bool act = i < h;
     warp_offer(w, wq, m, act ? __ldg(m + i) : 0.f, (uint32_t)i, act, K, nx, ny, nz, &cta_thr);
+    while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
   }
   const float4* m4 = reinterpret_cast<const float4*>(m + h);
   const int64_t n4 = (G - h) / 4;
@@ -182,12 +188,14 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
       warp_offer(w, wq, m, q[u].y, i + 1, act, K, nx, ny, nz, &cta_thr);
       warp_offer(w, wq, m, q[u].z, i + 2, act, K, nx, ny, nz, &cta_thr);
       warp_offer(w, wq, m, q[u].w, i + 3, act, K, nx, ny, nz, &cta_thr);
+      while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
     }
   }
   for (int64_t b = h + 4 * n4; b < G; b += kTopkThreads) {
     const int64_t i = b + threadIdx.x;
     const bool act = i < G;
     warp_offer(w, wq, m, act ? __ldg(m + i) : 0.f, (uint32_t)i, act, K, nx, ny, nz, &cta_thr);
+    while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
   }
   while (w.qn > 0) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
   if (lane < K) lists[warp][lane] = lane < w.cnt ? w.e : 0ull;
