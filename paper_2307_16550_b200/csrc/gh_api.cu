@@ -111,12 +111,14 @@ void free_table(gh::Table* t) {
   cudaFree(t->txrx_d);
   cudaFree(t->idx_d);
   cudaFree(t->coef_d);
-  cudaFree(t->plan.tiles_d);
-  cudaFree(t->plan.win_d);
-  cudaFree(t->plan.rows_d);
-  cudaFree(t->plan.coef3_d);
-  cudaFree(t->plan.binid_d);
-  cudaFree(t->plan.crow_d);
+  for (gh::Plan* pl : {&t->plan, &t->plan_map}) {
+    cudaFree(pl->tiles_d);
+    cudaFree(pl->win_d);
+    cudaFree(pl->rows_d);
+    cudaFree(pl->coef3_d);
+    cudaFree(pl->binid_d);
+    cudaFree(pl->crow_d);
+  }
   delete t;
 }
 
@@ -126,9 +128,8 @@ void check_combine(int combine) {
 
 // spectra in the gather layout for table t, from frames or from synthesis
 void* gather_spectra(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp,
-                     int T, int combine) {
-  gh::build_plan(c, t);
-  const gh::Plan& pl = t->plan;
+                     int T, int combine, bool mapmode) {
+  const gh::Plan& pl = gh::build_plan(c, t, mapmode);
   const int n_tb = (T + pl.tb - 1) / pl.tb;
   const size_t bytes = static_cast<size_t>(n_tb) * t->P * t->M * pl.tb * pl.esize;
   void* spec = c->spectra.get(bytes);
@@ -140,7 +141,7 @@ void* gather_spectra(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::S
 
 void hop_argmax(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
                 int combine, int64_t* idx_d, float* val_d) {
-  void* spec = gather_spectra(c, t, frames, sp, T, combine);
+  void* spec = gather_spectra(c, t, frames, sp, T, combine, false);
   auto* keys = static_cast<unsigned long long*>(c->keys.get(sizeof(unsigned long long) * T));
   GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * T, c->stream));
   gh::launch_gather(c, t, spec, T, combine, nullptr, keys);
@@ -179,8 +180,7 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
 // gather launches fill the GPU), then k_topk_localmax picks the peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
-  gh::build_plan(c, t);
-  const int tb = t->plan.tb;
+  const int tb = gh::build_plan(c, t, true).tb;
   int64_t chunk = (int64_t(1) << 31) / std::max<int64_t>(t->G, 1);
   chunk = std::max<int64_t>(tb, chunk / tb * tb);
   chunk = std::min<int64_t>(chunk, (T + tb - 1) / tb * tb);
@@ -195,7 +195,7 @@ void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthPar
       spc = &sc;
     }
     const float2* fr = frames ? frames + (int64_t)t0 * t->P * t->N : nullptr;
-    void* spec = gather_spectra(c, t, fr, spc, tc, combine);
+    void* spec = gather_spectra(c, t, fr, spc, tc, combine, true);
     gh::launch_gather(c, t, spec, tc, combine, map, nullptr);
     // the table's (shard) lattice: its layers only; peaks reported globally
     gh_grid lg = t->grid;
@@ -214,8 +214,7 @@ void hop_mc(gh::Ctx* c, gh::Table* t, const float2* frames, int T, int Mc, float
             int64_t* idx_d, float* val_d) {
   if (t->K != 1)
     fail(GH_EINVAL, "hop: multi-chirp frames need a K = 1 (nearest) table");
-  gh::build_plan(c, t);
-  const gh::Plan& pl = t->plan;
+  const gh::Plan& pl = gh::build_plan(c, t, map_d != nullptr);
   const int64_t per_trial = (int64_t)t->P * Mc * t->M;  // complex64 spectra
   int64_t chunk = (int64_t(1) << 29) / std::max<int64_t>(per_trial, 1);
   chunk = std::max<int64_t>(pl.tb, chunk / pl.tb * pl.tb);
@@ -735,7 +734,7 @@ int gh_hop_map_d(gh_ctx* ctx, gh_table* table, const float* frames_d, int32_t n_
     if (n_trials == 0) return;
     use_device(c);
     void* spec = gather_spectra(c, t, reinterpret_cast<const float2*>(frames_d), nullptr,
-                                n_trials, combine);
+                                n_trials, combine, true);
     gh::launch_gather(c, t, spec, n_trials, combine, map_d, nullptr);
   });
 }

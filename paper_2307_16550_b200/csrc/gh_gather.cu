@@ -68,7 +68,8 @@ struct GatherArgs {
 __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDesc& td,
                                               int64_t entry0, int64_t lb) {
   if (a.full) return a.binid ? (int64_t)__ldg(a.binid + entry0 + lb) : a.bin0 + entry0 + lb;
-  const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
+  int64_t lx, ly, lz;
+  tile_local(td, lb, &lx, &ly, &lz);
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
 }
 
@@ -320,13 +321,19 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
   }
   if constexpr (!MAPMODE) {
+    // exact ties go to the smaller bin: entry order is bin order on full
+    // plans (duplicate-row bins last) and plain tiles, not in 4 x 2 blocks
+    auto before = [&](int x, int y) {
+      if constexpr (FULL) return x < y;
+      else return global_bin(a, td, entry0, x) < global_bin(a, td, entry0, y);
+    };
     // merge the BPW lane groups of the warp (same trials, different bins)
 #pragma unroll
     for (int i = 0; i < TPL; ++i) {
       for (int o = L; o < 32; o <<= 1) {
         const float ov = __shfl_xor_sync(0xffffffffu, best[i], o);
         const int oi = __shfl_xor_sync(0xffffffffu, blb[i], o);
-        if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && oi < blb[i]))) {
+        if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && before(oi, blb[i])))) {
           best[i] = ov;
           blb[i] = oi;
         }
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
         const float val = red_v[w * TB + threadIdx.x];
         const int i = red_i[w * TB + threadIdx.x];
         if (i < 0) continue;
-        if (bi < 0 || val > bv || (val == bv && i < bi)) {
+        if (bi < 0 || val > bv || (val == bv && before(i, bi))) {
           bv = val;
           bi = i;
         }
@@ -546,6 +553,9 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
       }
     }
     if constexpr (!MAPMODE) {
+      auto before = [&](int x, int y) {  // exact ties: the smaller bin
+        return global_bin(a, td, entry0, x) < global_bin(a, td, entry0, y);
+      };
       // merge the warp's lane groups, then the warps (red buffers alternate
       // by item, so one barrier per item suffices)
       float* rv = red_v[it & 1u];
@@ -555,7 +565,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
         for (int o = L; o < 32; o <<= 1) {
           const float ov = __shfl_xor_sync(0xffffffffu, best[i], o);
           const int oi = __shfl_xor_sync(0xffffffffu, blb[i], o);
-          if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && oi < blb[i]))) {
+          if (oi >= 0 && (blb[i] < 0 || ov > best[i] || (ov == best[i] && before(oi, blb[i])))) {
             best[i] = ov;
             blb[i] = oi;
           }
@@ -573,7 +583,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
           const float val = rv[w * TB + threadIdx.x];
           const int i = ri[w * TB + threadIdx.x];
           if (i < 0) continue;
-          if (bi < 0 || val > bv || (val == bv && i < bi)) {
+          if (bi < 0 || val > bv || (val == bv && before(i, bi))) {
             bv = val;
             bi = i;
           }
@@ -688,7 +698,8 @@ void dispatch(Ctx* ctx, const GatherArgs& a, dim3 grid, size_t smem, bool mag, b
 
 void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, float* map_d,
                    unsigned long long* keys_d) {
-  const Plan& pl = t->plan;
+  const Plan& pl = map_d ? t->plan_map : t->plan;  // built by the caller (build_plan)
+  if (!pl.built) fail(GH_ERUNTIME, "gather: plan not built");
   GatherArgs a{};
   a.spec = spec_d;
   a.tiles = pl.tiles_d;

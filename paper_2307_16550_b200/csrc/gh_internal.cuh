@@ -128,8 +128,29 @@ struct TileDesc {
   int32_t x0, y0, z0, wx, wy, wz;
   int64_t entry_off;  // first entry (bin) of this tile in the plan arrays
   int32_t rows;       // staged rows in total (sum over pairs)
-  int32_t pad;
+  int32_t blk;        // 1: entries in 4 x 2 (x, y) blocks (wx % 4 == wy % 2 == 0)
 };
+
+// Local entry lb of a tile -> tile coordinates. Plain tiles run x-fastest;
+// blocked tiles (8-trial power plans) run 4 x 2 blocks x-fastest, 8 entries
+// each, so a half-warp of the gather (8 bins) reads a 4 x 2 patch: the
+// pairs' rows then advance along both axes and spread over the four bank
+// quarters of a 128-byte line (2 of them, not 4-8, collide per quarter, as a
+// run of 8 bins along x does when a pair's range grows 2 rows per bin). A
+// lane's own bins still come in increasing global order.
+__host__ __device__ __forceinline__ void tile_local(const TileDesc& td, int64_t lb, int64_t* lx,
+                                                    int64_t* ly, int64_t* lz) {
+  if (td.blk) {
+    const int64_t b = lb >> 3, w = lb & 7, nbx = td.wx >> 2, nby = td.wy >> 1;
+    *lx = 4 * (b % nbx) + (w & 3);
+    *ly = 2 * ((b / nbx) % nby) + (w >> 2);
+    *lz = b / (nbx * nby);
+  } else {
+    *lx = lb % td.wx;
+    *ly = (lb / td.wx) % td.wy;
+    *lz = lb / ((int64_t)td.wx * td.wy);
+  }
+}
 
 struct Plan {
   bool built = false;
@@ -165,7 +186,8 @@ struct Table {
   uint32_t* idx_d = nullptr;  // [G][P][K]
   double2* coef_d = nullptr;  // [G][P][K]
   double max_residual = 0.0;
-  Plan plan;
+  Plan plan;      // argmax gathers (tiled power plans: 4 x 2 blocked entries)
+  Plan plan_map;  // map-mode gathers (plain x-fastest entries: contiguous map stores)
 };
 
 // ------------------------------------------------------------ device helpers
@@ -228,7 +250,9 @@ void launch_chirp_power(Ctx* ctx, const float2* spec_d, int T, int P, int Mc, in
 void launch_synth(Ctx* ctx, const SynthParams& sp, int T, int P, int N, float2* frames_d,
                   double* truth_d);
 void build_table_device(Ctx* ctx, Table* t, int wrap);
-void build_plan(Ctx* ctx, Table* t);
+// the gather plan of a table for argmax (mapmode = false) or map-writing
+// gathers, built on first use
+Plan& build_plan(Ctx* ctx, Table* t, bool mapmode = false);
 void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
                    float* map_d, unsigned long long* keys_d);
 void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,

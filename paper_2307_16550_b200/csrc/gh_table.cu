@@ -256,7 +256,8 @@ __global__ void k_next_flag(const uint8_t* flags, int64_t total, int64_t after,
 // ---------------------------------------------------------------- plan
 
 __device__ inline void tile_bin(const TileDesc& td, const gh_grid& g, int64_t lb, int64_t* gb) {
-  const int64_t lx = lb % td.wx, ly = (lb / td.wx) % td.wy, lz = lb / ((int64_t)td.wx * td.wy);
+  int64_t lx, ly, lz;
+  tile_local(td, lb, &lx, &ly, &lz);
   *gb = (td.x0 + lx) + (int64_t)g.n[0] * ((td.y0 + ly) + (int64_t)g.n[1] * (td.z0 + lz));
 }
 
@@ -368,8 +369,7 @@ constexpr size_t kTileBudget = 216 * 1024;   // tiled plans: one CTA per SM
 // wherever possible (greedy matching of vector v with ~v within windows of
 // 1024 bins); `binid` maps entries back to bins, which keeps reported
 // indices and the smallest-bin tie rule exact.
-void permute_for_banks(Ctx* ctx, Table* t) {
-  Plan& pl = t->plan;
+void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   const int P = t->P, p4 = pl.p4, L = pl.tb * pl.esize / 16;
   const int64_t n = pl.n_entries;
   std::vector<uint16_t> rows(static_cast<size_t>(n) * p4), wm(rows.size());
@@ -554,9 +554,9 @@ void build_table_device(Ctx* ctx, Table* t, int wrap) {
   if (code) fail(code, err);
 }
 
-void build_plan(Ctx* ctx, Table* t) {
-  Plan& pl = t->plan;
-  if (pl.built) return;
+Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
+  Plan& pl = mapmode ? t->plan_map : t->plan;
+  if (pl.built) return pl;
   const int P = t->P, M = t->M;
   pl.k3 = t->K > 1;
   pl.esize = pl.k3 ? 8 : 4;
@@ -596,6 +596,10 @@ void build_plan(Ctx* ctx, Table* t) {
     // gather (17-64 pairs: 16 pairs = 4 row-table words per chunk); one
     // chunk otherwise
     pl.chunk_pairs = pl.p4 > 16 ? 16 : pl.p4;
+    // 8-trial power rows (32 bytes): entries in 4 x 2 blocks (tile_local)
+    // (argmax plans only: map-mode gathers store each trial's bins
+    // contiguously along x, which the plain order keeps)
+    const bool blocked = !mapmode && !pl.k3 && pl.tb == 8;
     const int n_chunks = (P + pl.chunk_pairs - 1) / pl.chunk_pairs;
     const int budget_rows = static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize));
     const int allow = budget_rows / P - 5;
@@ -623,6 +627,10 @@ void build_plan(Ctx* ctx, Table* t) {
         w[d] = std::min(w[d], g.n[d]);
       }
       if (dims == 2) w[2] = 1;
+      if (blocked) {  // whole 4 x 2 blocks (edge tiles may still be ragged)
+        if (w[0] >= 4) w[0] &= ~3;
+        if (w[1] >= 2) w[1] &= ~1;
+      }
       // the shard's box: layers [slab_lo, slab_hi) of z (3-D) or y (2-D)
       const int z_lo = dims == 3 ? t->slab_lo : 0, z_hi = dims == 3 ? t->slab_hi : g.n[2];
       const int y_lo = dims == 3 ? 0 : t->slab_lo, y_hi = dims == 3 ? g.n[1] : t->slab_hi;
@@ -638,6 +646,7 @@ void build_plan(Ctx* ctx, Table* t) {
             td.wy = std::min(w[1], y_hi - y);
             td.wz = std::min(w[2], z_hi - z);
             td.entry_off = off;
+            td.blk = blocked && td.wx % 4 == 0 && td.wy % 2 == 0;
             off += (int64_t)td.wx * td.wy * td.wz;
             tl.tiles.push_back(td);
           }
@@ -767,8 +776,9 @@ void build_plan(Ctx* ctx, Table* t) {
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(err_d);
   if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
-  if (pl.full && !pl.k3 && P <= 8) permute_for_banks(ctx, t);
+  if (pl.full && !pl.k3 && P <= 8) permute_for_banks(ctx, t, pl);
   pl.built = true;
+  return pl;
 }
 
 }  // namespace gh
