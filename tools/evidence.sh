@@ -26,6 +26,9 @@ python tools/prof_step.py --path direct --trials 1024 --steps 1 > $O/plain2.log 
 python tools/prof_step.py --config c3 --path topk --trials 2048 --steps 1 > $O/plain3.log 2>&1 && \
   ncu -f --set full --clock-control none --import-source on -k regex:"k_gather|k_fft|k_topk" -c 3 \
   -o $E/prof_c3_$R python tools/prof_step.py --config c3 --path topk --trials 2048 --steps 1 > $O/ncu3.log 2>&1
+python tools/prof_step.py --config c5 --trials 64 --steps 1 > $O/plain5.log 2>&1 && \
+  ncu -f --set full --clock-control none --import-source on -k regex:"k_gather" -c 1 \
+  -o $E/prof_c5_$R python tools/prof_step.py --config c5 --trials 64 --steps 1 > $O/ncu5.log 2>&1
 python tools/ncu_summary.py $E/*.ncu-rep --launches $O/launches_$R.csv --out $O/kernels_$R.json > /dev/null
 for f in $E/*.ncu-rep; do
   b=$(basename $f .ncu-rep)
