@@ -65,11 +65,20 @@ struct GatherArgs {
   unsigned long long* keys;
 };
 
+// PLAIN: the plan is known to run x-fastest (map-mode plans), so the
+// per-bin map stores skip the blocked-order decode
+template <bool PLAIN = false>
 __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDesc& td,
                                               int64_t entry0, int64_t lb) {
   if (a.full) return a.binid ? (int64_t)__ldg(a.binid + entry0 + lb) : a.bin0 + entry0 + lb;
   int64_t lx, ly, lz;
-  tile_local(td, lb, &lx, &ly, &lz);
+  if (PLAIN) {
+    lx = lb % td.wx;
+    ly = (lb / td.wx) % td.wy;
+    lz = lb / ((int64_t)td.wx * td.wy);
+  } else {
+    tile_local(td, lb, &lx, &ly, &lz);
+  }
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
 }
 
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
       }
       if (!check || j < nblk) {
         if constexpr (MAPMODE) {
-          const int64_t gb = global_bin(a, td, entry0, lb);
+          const int64_t gb = global_bin<true>(a, td, entry0, lb);
 #pragma unroll
           for (int i = 0; i < TPL; ++i) {
             const int trial = tb * TB + v * TPL + i;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   }
   if constexpr (!MAPMODE) {
     // exact ties go to the smaller bin: entry order is bin order on full
-    // plans (duplicate-row bins last) and plain tiles, not in 4 x 2 blocks
+    // plans (duplicate-row bins last) and plain tiles, not in 8-bin blocks
     auto before = [&](int x, int y) {
       if constexpr (FULL) return x < y;
       else return global_bin(a, td, entry0, x) < global_bin(a, td, entry0, y);
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
           vals[1] = acc[s][0].y;
         }
         if constexpr (MAPMODE) {
-          const int64_t gb = global_bin(a, td, entry0, lb);
+          const int64_t gb = global_bin<true>(a, td, entry0, lb);
 #pragma unroll
           for (int i = 0; i < TPL; ++i) {
             const int trial = tb * TB + v * TPL + i;

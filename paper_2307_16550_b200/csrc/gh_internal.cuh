@@ -128,23 +128,25 @@ struct TileDesc {
   int32_t x0, y0, z0, wx, wy, wz;
   int64_t entry_off;  // first entry (bin) of this tile in the plan arrays
   int32_t rows;       // staged rows in total (sum over pairs)
-  int32_t blk;        // 1: entries in 4 x 2 (x, y) blocks (wx % 4 == wy % 2 == 0)
+  int32_t blk;        // 0: plain order; else 1 + log2 of the 8-bin block's (x, y, z)
+                      // extents at bits 0-1, 2-3, 4-5 (extents divide wx, wy, wz)
 };
 
 // Local entry lb of a tile -> tile coordinates. Plain tiles run x-fastest;
-// blocked tiles (8-trial power plans) run 4 x 2 blocks x-fastest, 8 entries
-// each, so a half-warp of the gather (8 bins) reads a 4 x 2 patch: the
-// pairs' rows then advance along both axes and spread over the four bank
-// quarters of a 128-byte line (2 of them, not 4-8, collide per quarter, as a
-// run of 8 bins along x does when a pair's range grows 2 rows per bin). A
-// lane's own bins still come in increasing global order.
+// blocked tiles (8-trial power argmax plans) run 8-bin blocks (2 x 4 x 1 on
+// 2-D grids, 2 x 1 x 4 on 3-D ones) x-fastest, so a half-warp of the gather
+// (8 bins) reads a compact patch: the pairs' rows then advance along two
+// axes and spread over the four bank quarters of a 128-byte line instead of
+// colliding as a run of 8 bins along x does when a pair's range grows ~2 or
+// ~4 rows per bin. A lane's own bins still come in increasing global order.
 __host__ __device__ __forceinline__ void tile_local(const TileDesc& td, int64_t lb, int64_t* lx,
                                                     int64_t* ly, int64_t* lz) {
   if (td.blk) {
-    const int64_t b = lb >> 3, w = lb & 7, nbx = td.wx >> 2, nby = td.wy >> 1;
-    *lx = 4 * (b % nbx) + (w & 3);
-    *ly = 2 * ((b / nbx) % nby) + (w >> 2);
-    *lz = b / (nbx * nby);
+    const int sx = (td.blk - 1) & 3, sy = ((td.blk - 1) >> 2) & 3, sz = (td.blk - 1) >> 4;
+    const int64_t b = lb >> 3, w = lb & 7, nbx = td.wx >> sx, nby = td.wy >> sy;
+    *lx = ((b % nbx) << sx) | (w & ((1 << sx) - 1));
+    *ly = (((b / nbx) % nby) << sy) | ((w >> sx) & ((1 << sy) - 1));
+    *lz = ((b / (nbx * nby)) << sz) | (w >> (sx + sy));
   } else {
     *lx = lb % td.wx;
     *ly = (lb / td.wx) % td.wy;
@@ -186,7 +188,7 @@ struct Table {
   uint32_t* idx_d = nullptr;  // [G][P][K]
   double2* coef_d = nullptr;  // [G][P][K]
   double max_residual = 0.0;
-  Plan plan;      // argmax gathers (tiled power plans: 4 x 2 blocked entries)
+  Plan plan;      // argmax gathers (tiled power plans: 8-bin blocked entries)
   Plan plan_map;  // map-mode gathers (plain x-fastest entries: contiguous map stores)
 };
 

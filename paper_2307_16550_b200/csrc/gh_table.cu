@@ -596,10 +596,13 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
     // gather (17-64 pairs: 16 pairs = 4 row-table words per chunk); one
     // chunk otherwise
     pl.chunk_pairs = pl.p4 > 16 ? 16 : pl.p4;
-    // 8-trial power rows (32 bytes): entries in 4 x 2 blocks (tile_local)
+    // 8-trial power rows (32 bytes): entries in 8-bin blocks (tile_local)
     // (argmax plans only: map-mode gathers store each trial's bins
     // contiguously along x, which the plain order keeps)
     const bool blocked = !mapmode && !pl.k3 && pl.tb == 8;
+    const bool grid3 = t->grid.n[2] > 1;
+    const int bext[3] = {2, grid3 ? 1 : 4, grid3 ? 4 : 1};  // 8-bin block extents
+    const int blk_code = 1 + 1 + ((grid3 ? 0 : 2) << 2) + ((grid3 ? 2 : 0) << 4);
     const int n_chunks = (P + pl.chunk_pairs - 1) / pl.chunk_pairs;
     const int budget_rows = static_cast<int>(kTileBudget / (static_cast<size_t>(pl.tb) * pl.esize));
     const int allow = budget_rows / P - 5;
@@ -627,10 +630,9 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
         w[d] = std::min(w[d], g.n[d]);
       }
       if (dims == 2) w[2] = 1;
-      if (blocked) {  // whole 4 x 2 blocks (edge tiles may still be ragged)
-        if (w[0] >= 4) w[0] &= ~3;
-        if (w[1] >= 2) w[1] &= ~1;
-      }
+      if (blocked)  // whole blocks (edge tiles may still be ragged)
+        for (int d = 0; d < 3; ++d)
+          if (w[d] >= bext[d]) w[d] -= w[d] % bext[d];
       // the shard's box: layers [slab_lo, slab_hi) of z (3-D) or y (2-D)
       const int z_lo = dims == 3 ? t->slab_lo : 0, z_hi = dims == 3 ? t->slab_hi : g.n[2];
       const int y_lo = dims == 3 ? 0 : t->slab_lo, y_hi = dims == 3 ? g.n[1] : t->slab_hi;
@@ -646,7 +648,10 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
             td.wy = std::min(w[1], y_hi - y);
             td.wz = std::min(w[2], z_hi - z);
             td.entry_off = off;
-            td.blk = blocked && td.wx % 4 == 0 && td.wy % 2 == 0;
+            td.blk = blocked && td.wx % bext[0] == 0 && td.wy % bext[1] == 0 &&
+                             td.wz % bext[2] == 0
+                         ? blk_code
+                         : 0;
             off += (int64_t)td.wx * td.wy * td.wz;
             tl.tiles.push_back(td);
           }
