@@ -378,6 +378,33 @@ def test_pipelined_tiled_gather(ctx, P, scheme, combine, T):
     assert torch.equal(idx, idx2) and torch.equal(val, val2)
 
 
+def test_blocked_plan_exact_ties_smallest_bin(ctx):
+    # a tiled 8-trial plan (12 pairs, N = 512) whose entries run in 2 x 4
+    # blocks, on a grid fine enough that neighbouring bins share every
+    # pair's range row: their sums are bit-identical, and the argmax must
+    # still return the smallest bin of a tied maximum (direct.cpp:55-62)
+    nx, ny, sp = 60, 48, 0.08
+    ox, oy = -sp * (nx - 1) / 2, -sp * (ny - 1) / 2
+    sc = S.small(P=12, N=512, os=4, nx=nx, ny=ny, scheme=S.NEAREST).with_(
+        grid_spacing=(sp, sp, 1.0), grid_origin=(ox, oy, 0.0),
+        area_lo=(ox - sp / 2, oy - sp / 2, 0.0), area_hi=(-ox + sp / 2, -oy + sp / 2, 0.0))
+    T = 64
+    fr, _ = O.synth(sc, 3, T)
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    t = gh.precompute_hop_table(ctx, sc)
+    idx = gh.hop_argmax(ctx, t, frames_to_dev(fr))[0].cpu().numpy()
+    assert_argmax_parity(ref, idx, "blocked plan")
+    m = gh.hop_decision_map(ctx, t, frames_to_dev(fr)).cpu().numpy()
+    ties = 0
+    for k in range(T):
+        top = np.flatnonzero(m[k] == m[k].max())  # exact ties on the device map
+        if len(top) > 1:
+            ties += 1
+            assert idx[k] == top[0], (k, idx[k], top[:4])
+    assert ties > 0, "scene produced no exact ties"
+
+
 def c5_reduced():
     # BASELINE c5 stations/waveform (64 pairs, N = 512, os = 4, 3-D grid
     # spacing 0.195 x 0.195 x 0.3125 m) on a 48 x 40 x 8 block of the grid
