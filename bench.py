@@ -534,17 +534,32 @@ def run_grid_sharded(args, world, rank, local):
     if dist:
         tdist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
     with ClockSampler(local) as clk:
         e0.record()
         for k in range(args.steps):
             step(k)
         e1.record()
         torch.cuda.synchronize()
+    launches = ctx.launches - launches0
     ms = D.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
     if dist:
         tdist.barrier()
+    # per-kernel CUDA events in a second pass of the same steps
+    smem_peak = ctx.smem_peak_gbps()
+    ctx.reset_timing()
+    ctx.set_timing(not args.no_kernel_timing)
+    for k in range(args.steps):
+        step(k)
+    ctx.synchronize()
+    ctx.set_timing(False)
+    g_ms, g_n = ctx.kernel_time("gather")
+    f_ms, _ = ctx.kernel_time("synth_fft")
     if rank == 0:
         units = T * sc.units_per_trial()
+        shard_units = units * (hi - lo) / sc.slab_axis_len()  # this rank's slab
+        g_launch = max(g_ms / max(g_n, 1), 1e-9)
+        lsu_bytes = shard_units / max(1, g_n // args.steps) * 4.0
         line = {
             "metric": METRIC, "value": units / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
@@ -557,6 +572,15 @@ def run_grid_sharded(args, world, rank, local):
                        "parallelism": f"grid-sharded x{world}"},
             "trials_per_s": T / (ms * 1e-3),
             "table_build_s_rank0": t_build,
+            "kernels_ms": {"synth_fft": f_ms / args.steps, "gather": g_ms / args.steps},
+            "roofline": {"bound": "smem", "achieved": lsu_bytes / (g_launch * 1e-3) / 1e9,
+                         "peak": smem_peak, "unit": "GB/s",
+                         "frac": lsu_bytes / (g_launch * 1e-3) / 1e9 / smem_peak,
+                         "kernel": "k_gather_tiled (64 pairs, fused argmax, blocked entries)",
+                         "launch_ms": g_launch, "traffic": None,
+                         "peak_source": "measured in-run (gh_measure_smem_peak, LDS.128 all SMs)",
+                         "algorithmic_bytes_per_launch": lsu_bytes},
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
