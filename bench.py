@@ -2,17 +2,23 @@
 """Benchmark of the grid-hopping hot path (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2]
+                  [--config c3]
 
-One step = one Monte-Carlo batch of the configuration's trials (c2: 10,000
-trials, 40,000 location bins x 3 TX-RX pairs) through the hop pipeline:
-zero-padded range FFT -> gather-accumulate through the mapping operator ->
-fused per-trial argmax. Inputs (complex64 beat signals) are resident in HBM
-before timing (`value`); `e2e` runs the reference-facing host call
-gh_hop_estimate on pinned complex128 frames with the copies inside the timed
-region. Multi-GPU: one process per GPU, each rank owns its own block of
-trials (weak scaling, no data-path collective); the step time is the max
-over ranks (NCCL all-reduce of the timing only).
+Default workload: BASELINE c3, the largest configuration that fits one GPU
+(the metric is not quoted on a config): 100,000 Monte-Carlo trials per GPU,
+10^6 location bins x 16 TX-RX pairs, N = 1024, M = 4096, 5 targets, top-5
+local-maximum peak pick. One step = one pass of the hop pipeline over the
+step's trials: zero-padded range FFT -> gather-accumulate through the mapping
+operator -> per-trial top-5 local maxima. Inputs (complex64 beat signals) are
+resident in HBM before timing (`value`); `e2e` runs the reference-facing host
+call gh_hop_estimate_topk on pinned complex128 frames with the copies inside
+the timed region. `--config c1|c2|c4` run the other trial-sharded configs
+(argmax), `--config c5` the location-grid-sharded 3-D config.
+
+Multi-GPU: one process per GPU (`--gpus N` re-launches itself under
+torch.distributed.run when not already a rank); each rank owns its own block
+of trials (weak scaling, no data-path collective); the step time is the max
+over ranks.
 
 The reference arm (`--impl reference`) times the CPU restatement of the
 reference pipeline (oracle/, fp64, parallel_for over trials on every host
@@ -51,6 +57,8 @@ def peaks() -> dict:
 # profiles/ supplies roofline.traffic (DRAM read + write per launch)
 GATHER_KERNEL = {"c1": "k_gather<16, 0, 0, 0, 3, 1", "c2": "k_gather<16, 0, 0, 0, 3, 1",
                  "c3": "k_gather<8, 0, 0, 1, 16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
+GATHER_LABEL = {"c1": "k_gather (fused argmax)", "c2": "k_gather (fused argmax)",
+                "c3": "k_gather (map mode) + k_topk_localmax", "c4": "k_gather (K = 3, fused argmax)"}
 
 
 def ncu_traffic(config: str, trials: int):
@@ -167,28 +175,40 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(sc, oi, oc, target_s: float = 30.0, kind: str = "port") -> dict:
+def _oracle_campaign(O, sc, oi, oc, trial0, n, nthr):
+    if sc.topk > 1:
+        return O.campaign_hop_topk(sc, oi, oc, trial0, n, sc.topk, threads=nthr)
+    return O.campaign_hop(sc, oi, oc, trial0, n, threads=nthr)
+
+
+def _pick_label(sc) -> str:
+    return f"top-{sc.topk} local maxima" if sc.topk > 1 else "argmax"
+
+
+def cpu_baseline(sc, oi, oc, target_s: float = 20.0, kind: str = "port") -> dict:
     """The oracle's per-trial pipeline (synth -> FFT -> hop scan in 1024-bin
-    chunks -> argmax) with parallel_for over trials on all host cores."""
+    chunks -> argmax / top-k) with parallel_for over trials on all host cores,
+    timed on the first trials of the campaign (a bounded sample)."""
     from oracle import oracle as O
     nthr = O.nthreads()
     n = max(nthr, 8)
     t0 = time.perf_counter()
-    O.campaign_hop(sc, oi, oc, 0, n, threads=nthr)
+    _oracle_campaign(O, sc, oi, oc, 0, n, nthr)
     dt = time.perf_counter() - t0
     n2 = int(max(nthr, min(2_000_000, n * target_s / max(dt, 1e-3))))
     t0 = time.perf_counter()
-    O.campaign_hop(sc, oi, oc, 0, n2, threads=nthr)
+    _oracle_campaign(O, sc, oi, oc, 0, n2, nthr)
     dt = time.perf_counter() - t0
     units = n2 * sc.units_per_trial()
     return {"value": units / dt, "unit": UNIT, "cores": nthr, "kind": kind,
             "trials_per_s": n2 / dt,
-            "sample": f"{n2} trials of {sc.name} (first {n2} of the campaign), "
-                      f"{dt:.1f} s, fp64, {nthr} threads"}
+            "sample": f"first {n2} trials of the {sc.name} campaign ({_pick_label(sc)}), "
+                      f"{dt:.1f} s, fp64, {nthr} threads; value = their bin*pair rate"}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU pipeline (oracle port)."""
+    """--impl reference: the reference's CPU pipeline (oracle port) on this
+    arm's config, rank 0 only (other ranks exit without work)."""
     if rank != 0:
         return
     from paper_2307_16550_b200 import scene as S
@@ -197,12 +217,17 @@ def run_reference(args, world, rank):
     oi, oc, _ = O.build_table(sc)
     nthr = O.nthreads()
     # bounded sample per step so that warmup + steps end within minutes
-    per_step = max(nthr, min(sc.trials, args.ref_trials))
+    t0 = time.perf_counter()
+    _oracle_campaign(O, sc, oi, oc, 0, nthr, nthr)
+    per_trial = (time.perf_counter() - t0) / nthr
+    budget = args.ref_seconds / max(1, args.steps + args.warmup)
+    per_step = int(max(nthr, min(sc.trials, args.ref_trials or 10**9, budget / max(per_trial, 1e-9))))
+    per_step = max(nthr, per_step // nthr * nthr)
     for _ in range(args.warmup):
-        O.campaign_hop(sc, oi, oc, 0, max(nthr, per_step // 4), threads=nthr)
+        _oracle_campaign(O, sc, oi, oc, 0, max(nthr, per_step // 4), nthr)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        O.campaign_hop(sc, oi, oc, k * per_step, per_step, threads=nthr)
+        _oracle_campaign(O, sc, oi, oc, k * per_step, per_step, nthr)
     dt = (time.perf_counter() - t0) / args.steps
     value = per_step * sc.units_per_trial() / dt
     line = {
@@ -210,12 +235,16 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (counter-based RNG, seed 20260816)",
-        "config": {"workload": f"{sc.name}: {per_step} trials/step sample of {sc.trials}",
+        "config": {"workload": f"{sc.name}: {per_step} trials/step sample of {sc.trials}, "
+                               f"{sc.n_bins} bins x {sc.n_pairs} pairs, N={sc.n_samples}, "
+                               f"M={sc.n_fft}, {S.SCHEME_NAMES[sc.scheme]} (K={sc.k}), "
+                               f"{_pick_label(sc)}",
                    "bins": sc.n_bins, "pairs": sc.n_pairs, "n_samples": sc.n_samples,
-                   "n_fft": sc.n_fft, "scheme": "nearest"},
+                   "n_fft": sc.n_fft, "scheme": S.SCHEME_NAMES[sc.scheme], "topk": sc.topk},
         "trials_per_s": per_step / dt,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthr, "kind": "port",
-                         "sample": f"{per_step} trials per step"},
+                         "sample": f"{per_step} trials per step (trials k*{per_step}.. of the "
+                                   f"campaign), fp64, {nthr} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference (Eigen3/FFTW3) not buildable here; fp64 oracle port of its "
                 "pipeline, parallel_for over trials on all host cores",
@@ -236,15 +265,17 @@ def run_ours(args, world, rank, local):
     sc = S.baseline(args.config)
     T = args.trials or sc.trials
     G, P, N = sc.n_bins, sc.n_pairs, sc.n_samples
+    dev = f"cuda:{local}"
     ctx = gh.Context(local)
     stream = ctx.torch_stream()
     table = gh.precompute_hop_table(ctx, sc)
     trial0 = rank * T  # weak scaling: every rank owns its own trials
     frames, _ = gh.synthesize(ctx, sc, trial0, T)
     ctx.synchronize()
-    # L2 is 126 MB: frames (61 MB) + spectra (123 MB) would partly stay
-    # resident, so L2 is flushed between timed steps (outside the events)
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+    # L2 is 126 MB: c1/c2 frames (61 MB) + spectra (123 MB) would partly stay
+    # resident, so L2 is flushed between timed steps (outside the events);
+    # the c3/c4 inputs (13 GB / 5 GB) exceed it anyway
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def barrier():
         if dist:
@@ -281,7 +312,7 @@ def run_ours(args, world, rank, local):
         ctx.synchronize()
         t_wall = time.perf_counter() - t_wall
     barrier()
-    launches = ctx.launches - launches0 - 0
+    launches = ctx.launches - launches0
     ms_steps = [a.elapsed_time(b) for a, b in evs]
     ms = sum(ms_steps) / len(ms_steps)
     ctx.reset_timing()
@@ -292,66 +323,79 @@ def run_ours(args, world, rank, local):
             step()
     ctx.synchronize()
     ctx.set_timing(False)
-    g_ms, g_n = ctx.kernel_time("gather")
-    f_ms, f_n = ctx.kernel_time("fft")
-    d_ms, d_n = ctx.kernel_time("decode")
-    k_ms, k_n = ctx.kernel_time("topk")
+    kern = {name: ctx.kernel_time(name) for name in ("fft", "gather", "decode", "topk", "merge")}
     if dist:
-        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
     units_step = T * G * P * world
     value = units_step / (ms * 1e-3)
     clocks = clk.summary()
 
-    # ---- e2e: reference-facing host call, pinned complex128 frames
+    # ---- e2e: reference-facing host call on pinned complex128 frames (the
+    # reference's FrameSet element type), H2D + D2H inside the timed region
+    kk = max(topk, 1)
     fr_host = torch.empty((T, P, N), dtype=torch.complex128, pin_memory=True)
-    fr_host.copy_(frames.cpu().to(torch.complex128))
-    idx_h = torch.empty(T, dtype=torch.int64, pin_memory=True)
-    val_h = torch.empty(T, dtype=torch.float64, pin_memory=True)
+    for a0 in range(0, T, 8192):
+        fr_host[a0:a0 + 8192].copy_(frames[a0:a0 + 8192].cpu())
+    idx_h = torch.empty((T, kk), dtype=torch.int64, pin_memory=True)
+    val_h = torch.empty((T, kk), dtype=torch.float64, pin_memory=True)
+
+    def e2e_step():
+        if topk:
+            gh.api.hop_estimate_topk_ptr(ctx, table, fr_host.data_ptr(), T, S.POWER, topk,
+                                         idx_h.data_ptr(), val_h.data_ptr())
+        else:
+            gh.api.hop_estimate_ptr(ctx, table, fr_host.data_ptr(), T, S.POWER, idx_h.data_ptr(),
+                                    val_h.data_ptr())
+
     for _ in range(2):
-        gh.api.hop_estimate_ptr(ctx, table, fr_host.data_ptr(), T, S.POWER, idx_h.data_ptr(),
-                                val_h.data_ptr())
+        e2e_step()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        gh.api.hop_estimate_ptr(ctx, table, fr_host.data_ptr(), T, S.POWER, idx_h.data_ptr(),
-                                val_h.data_ptr())
+        e2e_step()
     e2e_s = (time.perf_counter() - t0) / args.steps
-    # this box's raw pinned H2D rate (one 123 MB-class copy), the bound e2e
-    # runs against when the frames cross PCIe as complex128
-    dst = torch.empty(fr_host.shape, dtype=fr_host.dtype, device=f"cuda:{local}")
-    dst.copy_(fr_host, non_blocking=True)
+    # this box's raw pinned H2D rate (a 1 GB copy), the bound e2e runs
+    # against when the frames cross PCIe as complex128
+    n_probe = min(T, max(1, (1 << 30) // (P * N * 16)))
+    dst = torch.empty((n_probe, P, N), dtype=fr_host.dtype, device=dev)
+    dst.copy_(fr_host[:n_probe], non_blocking=True)
     torch.cuda.synchronize()
     h0 = time.perf_counter()
     for _ in range(3):
-        dst.copy_(fr_host, non_blocking=True)
+        dst.copy_(fr_host[:n_probe], non_blocking=True)
     torch.cuda.synchronize()
-    h2d_gbs = 3 * fr_host.numel() * fr_host.element_size() / (time.perf_counter() - h0) / 1e9
+    h2d_gbs = 3 * dst.numel() * dst.element_size() / (time.perf_counter() - h0) / 1e9
     del dst
     if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         e2e_s = float(t.item())
     # same answers through both entry points
-    top1 = idx[:, 0] if topk else idx  # the global argmax is the first local maximum
-    assert np.array_equal(idx_h.numpy(), top1.cpu().numpy())
+    assert np.array_equal(idx_h.numpy().reshape(T, -1), idx.cpu().numpy().reshape(T, -1))
+    del fr_host
 
     # ---- Monte-Carlo campaign step (synthesis fused into the FFT)
+    def camp_step():
+        if topk:
+            return gh.campaign_hop_topk(ctx, table, sc, trial0, T, topk)
+        return gh.campaign_hop(ctx, table, sc, trial0, T)
+
     for _ in range(2):
-        gh.campaign_hop(ctx, table, sc, trial0, T)
+        camp_step()
     ctx.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
         for k in range(args.steps):
-            gh.campaign_hop(ctx, table, sc, trial0, T)
+            camp_step()
         e1.record(stream)
     ctx.synchronize()
     camp_ms = e0.elapsed_time(e1) / args.steps
 
-    # ---- direct method (BASELINE c2 "run both ways"): tcgen05 3xTF32
+    # ---- direct method (BASELINE c2 "run both ways"): tcgen05 3xFP16
     direct = None
     if not args.no_direct and sc.name in ("c1", "c2"):
         for _ in range(2):
@@ -421,19 +465,20 @@ def run_ours(args, world, rank, local):
             tdist.destroy_process_group()
         return
     pk = peaks()
+    g_ms, g_n = kern["gather"]
     g_avg = g_ms / args.steps  # per step (top-K steps run the gather once per trial chunk)
+    # per launch (top-K steps may launch the gather once per trial chunk)
+    g_launches = max(1, g_n // args.steps)
+    t_launch = T / g_launches
+    g_launch_ms = max(g_avg / g_launches, 1e-9)  # (no kernel timing: diagnostic runs only)
     # shared-memory bytes gathered per unit: fp32 power (K = 1) or three
     # complex64 spectrum values (K = 3)
-    # per launch (top-K steps launch the gather once per trial chunk)
-    g_launches = max(1, g_n // args.steps)
-    t_launch = T // g_launches
-    g_launch_ms = g_avg / g_launches
     lsu_bytes = t_launch * G * P * (4.0 if sc.k == 1 else 24.0)
-    g_launch_ms = max(g_launch_ms, 1e-9)  # (no kernel timing: diagnostic runs only)
     achieved = lsu_bytes / (g_launch_ms * 1e-3) / 1e9
     # staged spectra (fp32 power, or complex64 for K = 3) + table rows
     hbm_bytes = (t_launch * P * sc.n_fft * (4.0 if sc.k == 1 else 8.0) + G * 8
                  + (G * P * 24 if sc.k == 3 else 0))
+    kernels_ms = {k: v[0] / args.steps for k, v in kern.items() if v[1]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
@@ -442,17 +487,17 @@ def run_ours(args, world, rank, local):
         "config": {"workload": f"{sc.name}: {T} trials/GPU, {G} bins x {P} pairs, N={N}, "
                                f"M={sc.n_fft}, {S.SCHEME_NAMES[sc.scheme]} (K={sc.k}), power sum, "
                                f"{'wrap mode' if sc.wrap else 'reference window check'}, "
-                               f"{f'top-{topk} local maxima' if topk else 'argmax'}",
+                               f"{_pick_label(sc)}",
                    "trials_per_gpu": T, "bins": G, "pairs": P, "n_fft": sc.n_fft,
+                   "topk": sc.topk,
                    "l2": "flushed between timed steps (512 MB write, outside the events)",
                    "parallelism": f"trial-sharded x{world}"},
         "trials_per_s": T * world / (ms * 1e-3),
         "wall_ms_per_step": t_wall * 1e3 / args.steps,
         "kernel_timing": "per-kernel CUDA events on the launching stream, in a second pass of "
                          "the same steps (the headline pass has only the step events)",
-        "kernels_ms": {"fft": f_ms / args.steps, "gather": g_avg, "decode": d_ms / args.steps,
-                       **({"topk": k_ms / args.steps} if topk else {})},
-        "launches_per_step": {"fft": f_n // args.steps, "gather": g_n // args.steps},
+        "kernels_ms": kernels_ms,
+        "launches_per_step": {k: v[1] / args.steps for k, v in kern.items() if v[1]},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak,
                      "traffic": ncu_traffic(sc.name, t_launch),
@@ -460,21 +505,25 @@ def run_ours(args, world, rank, local):
                      "traffic_note": "DRAM read+write bytes per launch from the committed ncu "
                                      "--set full capture (profiles/), compare with hbm."
                                      "bytes_per_launch",
-                     "kernel": (f"k_gather (map mode; top-{topk} local maxima by k_topk_localmax)"
-                                if topk else "k_gather (fused argmax)"),
+                     "kernel": GATHER_LABEL.get(sc.name, "k_gather"),
                      "peak_source": "measured in-run (gh_measure_smem_peak, LDS.128 all SMs)",
                      "algorithmic_bytes_per_launch": lsu_bytes,
+                     "unit_bytes": "4 B of shared-memory power per bin x pair x trial (K = 1), "
+                                   "24 B (3 complex64) for K = 3",
                      "hbm": {"bytes_per_launch": hbm_bytes,
                              "achieved_gbs": hbm_bytes / (g_launch_ms * 1e-3) / 1e9,
                              "peak_gbs": pk.get("hbm_gbs")}},
         "e2e": {"value": units_step / e2e_s, "unit": UNIT,
-                "h2d_bytes_per_step": T * P * N * 16, "d2h_bytes_per_step": T * (8 + 4),
-                "ms_per_step": e2e_s * 1e3, "api": "gh_hop_estimate (host complex128 frames)",
+                "h2d_bytes_per_step": T * P * N * 16, "d2h_bytes_per_step": T * kk * (8 + 4),
+                "ms_per_step": e2e_s * 1e3,
+                "api": ("gh_hop_estimate_topk" if topk else "gh_hop_estimate")
+                       + " (host complex128 frames, pinned)",
                 "h2d_gbs_raw": h2d_gbs,
                 "h2d_bound_ms": T * P * N * 16 / (h2d_gbs * 1e9) * 1e3},
         "campaign": {"ms_per_step": camp_ms, "trials_per_s": T * world / (camp_ms * 1e-3),
                      "value": units_step / (camp_ms * 1e-3),
-                     "api": "gh_campaign_hop_d (synthesis fused into the FFT)"},
+                     "api": ("gh_campaign_hop_topk_d" if topk else "gh_campaign_hop_d")
+                            + " (synthesis fused into the FFT)"},
         "gpu_launches": launches,
         "clocks": clocks,
     }
@@ -588,21 +637,39 @@ def run_grid_sharded(args, world, rank, local):
         tdist.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """`--gpus N` outside torch.distributed.run: start one rank per GPU
+    (127.0.0.1 rendezvous) and return their exit status."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--trials", type=int, default=0)
-    ap.add_argument("--ref-trials", type=int, default=4000)
+    ap.add_argument("--ref-trials", type=int, default=0,
+                    help="reference arm: cap on trials per step (default: time-bounded)")
+    ap.add_argument("--ref-seconds", type=float, default=90.0,
+                    help="reference arm: CPU seconds for warmup + steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-direct", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="diagnostic: no per-kernel CUDA events inside the timed steps")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)

@@ -279,6 +279,11 @@ int gh_hop_argmax_d(gh_ctx* ctx, gh_table* t, const float* frames_d,
 int gh_hop_estimate(gh_ctx* ctx, gh_table* t, const double* frames,
                     int32_t n_trials, int32_t combine, int64_t* idx,
                     double* val);
+/* Multi-target form from HOST complex128 frames (BASELINE c3): the top-k
+ * local maxima of gh_hop_topk_d, idx int64 [T][k] (-1 = none), val fp64
+ * [T][k]; copies are inside the call, pipelined with the compute. */
+int gh_hop_estimate_topk(gh_ctx* ctx, gh_table* t, const double* frames, int32_t n_trials,
+                         int32_t combine, int32_t k, int64_t* idx, double* val);
 /* Monte-Carlo campaign step (src/montecarlo.cpp:140-175, hop arm): synth
  * fused into the FFT, then gather + argmax; nothing but results touch HBM. */
 int gh_campaign_hop_d(gh_ctx* ctx, gh_table* t, const gh_campaign* camp,

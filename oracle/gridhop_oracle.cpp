@@ -1087,6 +1087,104 @@ int or_campaign_hop(const or_wave* w, const or_grid* g, const or_campaign* c,
   });
 }
 
+// Top-k local maxima per trial (BASELINE c3/c5 multi-target campaigns): the
+// hop pipeline of or_campaign_hop, then or_topk_local_max on each map.
+int or_campaign_hop_topk(const or_wave* w, const or_grid* g, const or_campaign* c,
+                         const uint32_t* idx, const double* coef, int32_t k, int magnitude,
+                         int wrap, uint64_t trial0, int32_t n_trials, int32_t topk,
+                         int n_threads, int64_t* est_idx, double* est_val) {
+  return guarded([&] {
+    check_wave(*w);
+    if (topk < 1 || topk > 8) throw std::invalid_argument("top-k: k must be in [1, 8]");
+    const int P = w->n_pairs, N = w->n_samples, M = N * w->os_range;
+    const int64_t G = grid_size(*g);
+    const std::vector<cplx> tw = twiddles(M);
+    std::string first_err;
+    parallel_for(n_trials, n_threads, [&](int64_t t) {
+      std::vector<double> frame(static_cast<size_t>(P) * N * 2);
+      std::vector<cplx> spec(static_cast<size_t>(P) * M);
+      std::vector<double> map(static_cast<size_t>(G));
+      synth_trial(*w, *c, trial0 + static_cast<uint64_t>(t), wrap, frame.data(), nullptr);
+      for (int p = 0; p < P; ++p)
+        dft_row(frame.data() + static_cast<size_t>(p) * N * 2, N, M,
+                spec.data() + static_cast<size_t>(p) * M, tw);
+      for (int64_t b0 = 0; b0 < G; b0 += 1024) {
+        const int64_t nb = std::min<int64_t>(1024, G - b0);
+        hop_map_trial(spec.data(), P, M, idx + static_cast<size_t>(b0) * P * k,
+                      coef + static_cast<size_t>(b0) * P * k * 2, nb, k, magnitude,
+                      map.data() + b0);
+      }
+      if (or_topk_local_max(map.data(), g, topk, est_idx + t * topk, est_val + t * topk) != 0)
+        throw std::runtime_error(g_err);
+    });
+  });
+}
+
+// Campaign statistics of one batch (run_monte_carlo's hit_ratio,
+// montecarlo.cpp:181-190, extended with location RMSE and K-target
+// assignment). Per trial, truths x_i (i < kt, rows of truth [T][kt][3]) are
+// matched to estimates (est [T][ke] grid bins, -1 = none) by the injective
+// assignment of least total squared distance over the permutations of
+// max(kt, ke) slots in lexicographic order (first minimum kept); an
+// unmatched truth counts at distance `miss_m`. Distances are formed as
+// sqrt((dx*dx + dy*dy) + dz*dz), every operation rounded separately.
+// out[0] += estimates counted, out[1 + j] += hits within thresholds[j],
+// out[1 + nth] += sum of squared distances, out[2 + nth] += hits within
+// half_res, out[3 + nth] += sum of distances. assign [T][kt] (nullable):
+// the estimate slot matched to each truth (-1 = missed).
+int or_trial_stats(const or_grid* g, const int64_t* est, int32_t ke, const double* truth,
+                   int32_t kt, int32_t n_trials, const double* thresholds, int32_t nth,
+                   double half_res, double miss_m, double* out, int32_t* assign) {
+  return guarded([&] {
+    const int n = std::max(ke, kt);
+    if (n < 1 || n > 6) throw std::invalid_argument("stats: at most 6 targets / estimates");
+    std::vector<int> perm(static_cast<size_t>(n)), bestp(static_cast<size_t>(n));
+    std::vector<double> dist(static_cast<size_t>(kt) * n);
+    for (int32_t t = 0; t < n_trials; ++t) {
+      for (int i = 0; i < kt; ++i)
+        for (int j = 0; j < n; ++j) {
+          const int64_t b = j < ke ? est[static_cast<int64_t>(t) * ke + j] : -1;
+          double d = miss_m;
+          if (b >= 0) {
+            double x[3];
+            grid_point(*g, b, x);
+            const double* tr = truth + (static_cast<int64_t>(t) * kt + i) * 3;
+            const double dx = x[0] - tr[0], dy = x[1] - tr[1], dz = x[2] - tr[2];
+            d = std::sqrt((dx * dx + dy * dy) + dz * dz);
+          }
+          dist[static_cast<size_t>(i) * n + j] = d;
+        }
+      for (int j = 0; j < n; ++j) perm[static_cast<size_t>(j)] = j;
+      double best = 0.0;
+      bool have = false;
+      do {
+        double cost = 0.0;
+        for (int i = 0; i < kt; ++i) {
+          const double d = dist[static_cast<size_t>(i) * n + perm[static_cast<size_t>(i)]];
+          cost = cost + d * d;
+        }
+        if (!have || cost < best) {
+          best = cost;
+          bestp = perm;
+          have = true;
+        }
+      } while (std::next_permutation(perm.begin(), perm.end()));
+      for (int i = 0; i < kt; ++i) {
+        const int j = bestp[static_cast<size_t>(i)];
+        const double d = dist[static_cast<size_t>(i) * n + j];
+        const bool matched = j < ke && est[static_cast<int64_t>(t) * ke + j] >= 0;
+        if (assign) assign[static_cast<int64_t>(t) * kt + i] = matched ? j : -1;
+        out[0] += 1.0;
+        for (int h = 0; h < nth; ++h)
+          if (d <= thresholds[h]) out[1 + h] += 1.0;
+        out[1 + nth] += d * d;
+        if (d <= half_res) out[2 + nth] += 1.0;
+        out[3 + nth] += d;
+      }
+    }
+  });
+}
+
 int or_campaign_direct(const or_wave* w, const or_grid* g, const or_campaign* c,
                        int magnitude, int wrap, uint64_t trial0, int32_t n_trials,
                        int n_threads, int64_t* est_idx, double* est_val) {

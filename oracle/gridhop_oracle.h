@@ -125,6 +125,15 @@ int or_campaign_hop(const or_wave* w, const or_grid* g, const or_campaign* c,
                     const uint32_t* idx, const double* coef, int32_t k,
                     int magnitude, int wrap, uint64_t trial0, int32_t n_trials,
                     int n_threads, int64_t* est_idx, double* est_val);
+int or_campaign_hop_topk(const or_wave* w, const or_grid* g, const or_campaign* c,
+                         const uint32_t* idx, const double* coef, int32_t k, int magnitude,
+                         int wrap, uint64_t trial0, int32_t n_trials, int32_t topk,
+                         int n_threads, int64_t* est_idx, double* est_val);
+/* Campaign statistics of a batch (hit_ratio, montecarlo.cpp:181-190, + RMSE
+ * and K-target assignment); see the definition for the layout of out. */
+int or_trial_stats(const or_grid* g, const int64_t* est, int32_t ke, const double* truth,
+                   int32_t kt, int32_t n_trials, const double* thresholds, int32_t nth,
+                   double half_res, double miss_m, double* out, int32_t* assign);
 int or_campaign_direct(const or_wave* w, const or_grid* g, const or_campaign* c,
                        int magnitude, int wrap, uint64_t trial0,
                        int32_t n_trials, int n_threads, int64_t* est_idx,

@@ -66,6 +66,10 @@ def lib():
             "or_multilaterate": (C.c_int, [P(CWave), P(CGrid), vp, i32, C.c_int, vp, vp]),
             "or_campaign_hop": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), vp, vp, i32, C.c_int,
                                           C.c_int, u64, i32, C.c_int, vp, vp]),
+            "or_campaign_hop_topk": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), vp, vp, i32,
+                                               C.c_int, C.c_int, u64, i32, i32, C.c_int, vp, vp]),
+            "or_trial_stats": (C.c_int, [P(CGrid), vp, i32, vp, i32, i32, vp, i32, f64, f64, vp,
+                                         vp]),
             "or_campaign_direct": (C.c_int, [P(CWave), P(CGrid), P(CCampaign), C.c_int, C.c_int,
                                              u64, i32, C.c_int, vp, vp]),
         }
@@ -264,3 +268,53 @@ def campaign_direct(scene, trial0: int, n_trials: int, snr_db=None, magnitude=Fa
                                     int(scene.wrap if wrap is None else wrap), trial0, n_trials,
                                     threads or nthreads(), ei.ctypes.data, ev.ctypes.data))
     return ei, ev
+
+
+def campaign_hop_topk(scene, idx, coef, trial0: int, n_trials: int, topk: int, snr_db=None,
+                      magnitude=False, wrap=None, threads: int | None = None):
+    """Top-k local maxima per trial of the hop map (BASELINE c3/c5): (idx [T, k], val [T, k])."""
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    coef = np.ascontiguousarray(coef, dtype=np.complex128)
+    K = idx.shape[-1]
+    ei = np.zeros((n_trials, topk), dtype=np.int64)
+    ev = np.zeros((n_trials, topk))
+    w, g, c = scene.c_wave(), scene.c_grid(), scene.c_campaign(snr_db)
+    _check(lib().or_campaign_hop_topk(C.byref(w), C.byref(g), C.byref(c), idx.ctypes.data,
+                                      coef.ctypes.data, K, int(magnitude),
+                                      int(scene.wrap if wrap is None else wrap), trial0, n_trials,
+                                      topk, threads or nthreads(), ei.ctypes.data, ev.ctypes.data))
+    return ei, ev
+
+
+DEFAULT_THRESHOLDS = tuple(0.2 * i for i in range(1, 16))  # scenario.cpp:177-179
+
+
+def half_resolution(scene) -> float:
+    """Half the range resolution c / (2 B) (model.hpp range_resolution)."""
+    return 0.5 * scene.c / (2.0 * scene.bandwidth)
+
+
+def miss_distance(scene) -> float:
+    """Distance charged to an unmatched target: the grid box diagonal."""
+    sp = np.asarray(scene.grid_spacing, dtype=np.float64)
+    n = np.asarray(scene.grid_n, dtype=np.float64)
+    return float(np.sqrt(np.sum((sp * n) ** 2)))
+
+
+def trial_stats(scene, est: np.ndarray, truth: np.ndarray, thresholds=DEFAULT_THRESHOLDS):
+    """or_trial_stats: (stats vector [4 + nth], assignment [T, kt]). est [T]
+    or [T, ke] grid bins (-1 = none); truth [T, kt, 3]."""
+    est = np.ascontiguousarray(est, dtype=np.int64)
+    if est.ndim == 1:
+        est = est[:, None]
+    truth = np.ascontiguousarray(truth, dtype=np.float64)
+    T, ke = est.shape
+    kt = truth.shape[1]
+    th = np.ascontiguousarray(thresholds, dtype=np.float64)
+    out = np.zeros(4 + th.size)
+    assign = np.zeros((T, kt), dtype=np.int32)
+    g = scene.c_grid()
+    _check(lib().or_trial_stats(C.byref(g), est.ctypes.data, ke, truth.ctypes.data, kt, T,
+                                th.ctypes.data, th.size, half_resolution(scene),
+                                miss_distance(scene), out.ctypes.data, assign.ctypes.data))
+    return out, assign

@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
             "gh_hop_map_d": (C.c_int, [vp, vp, vp, i32, i32, vp]),
             "gh_hop_argmax_d": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
             "gh_hop_estimate": (C.c_int, [vp, vp, vp, i32, i32, vp, vp]),
+            "gh_hop_estimate_topk": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
             "gh_campaign_hop_d": (C.c_int, [vp, vp, P(CCampaign), u64, i32, i32, vp, vp]),
             "gh_hop_topk_d": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
             "gh_campaign_hop_topk_d": (C.c_int, [vp, vp, P(CCampaign), u64, i32, i32, i32, vp, vp]),
@@ -393,7 +394,7 @@ def indirect_argmin(ctx: Context, scene: Scene, frames):
     """Indirect pipeline location stage (src/indirect.cpp:10-83, Mc = 1):
     (r_hat fp64 [T, P], bin int64 [T], residual fp64 [T])."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _scene_frames(scene, frames)
     T = frames.shape[0]
     dev = frames.device
     rhat = torch.empty((T, scene.n_pairs), dtype=torch.float64, device=dev)
@@ -466,11 +467,34 @@ def table_load(ctx: Context, path: str, scene: Scene, scene_hash: int) -> HopTab
     return HopTable(ctx, scene, h)
 
 
-def _as_float_frames(frames):
+def _as_float_frames(frames, n_pairs: int | None = None, n_samples: int | None = None):
+    """Device frames complex64 [T, P, N]; with (n_pairs, n_samples) given the
+    per-trial shape must match ("hop: frame shape mismatch",
+    src/hopping.cpp:251) — the C ABI takes only T and reads P*N per trial."""
     torch = _torch()
     if frames.dtype != torch.complex64 or not frames.is_cuda or not frames.is_contiguous():
         raise InvalidArgument("frames must be a contiguous CUDA complex64 tensor [T, P, N]")
+    if frames.dim() != 3:
+        raise InvalidArgument("hop: frame shape mismatch")
+    if n_pairs is not None and (frames.shape[1] != n_pairs or frames.shape[2] != n_samples):
+        raise InvalidArgument("hop: frame shape mismatch")
     return frames
+
+
+def _table_frames(table: "HopTable", frames):
+    return _as_float_frames(frames, table.n_pairs, table.scene.n_samples)
+
+
+def _scene_frames(scene: Scene, frames):
+    return _as_float_frames(frames, scene.n_pairs, scene.n_samples)
+
+
+def _as_maps(scene: Scene, maps):
+    torch = _torch()
+    if (maps.dtype != torch.float32 or not maps.is_cuda or maps.dim() != 2
+            or maps.shape[1] != scene.n_bins):
+        raise InvalidArgument("top-k: maps must be a CUDA float32 tensor [T, n_bins]")
+    return maps.contiguous()
 
 
 def synthesize(ctx: Context, scene: Scene, trial0: int, n_trials: int, snr_db=None,
@@ -501,7 +525,7 @@ def fast_time_spectra(ctx: Context, frames, os_range: int):
 def hop_decision_map(ctx: Context, table: HopTable, frames, combine: int = POWER):
     """hop_decision_map (src/hopping.cpp:179-183) for T trials: fp32 [T, G]."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _table_frames(table, frames)
     out = torch.empty((frames.shape[0], table.n_bins), dtype=torch.float32, device=frames.device)
     _check(lib().gh_hop_map_d(ctx.h, table.h, _ptr(frames), frames.shape[0], combine, _ptr(out)))
     return out
@@ -510,7 +534,7 @@ def hop_decision_map(ctx: Context, table: HopTable, frames, combine: int = POWER
 def hop_argmax(ctx: Context, table: HopTable, frames, combine: int = POWER):
     """hop_estimate location stage (src/hopping.cpp:238-267) batched: (idx, value)."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _table_frames(table, frames)
     T = frames.shape[0]
     idx = torch.empty(T, dtype=torch.int64, device=frames.device)
     val = torch.empty(T, dtype=torch.float32, device=frames.device)
@@ -538,6 +562,28 @@ def hop_estimate_ptr(ctx: Context, table: HopTable, frames_ptr: int, n_trials: i
     _check(lib().gh_hop_estimate(ctx.h, table.h, frames_ptr, n_trials, combine, idx_ptr, val_ptr))
 
 
+def hop_estimate_topk(ctx: Context, table: HopTable, frames: np.ndarray, k: int,
+                      combine: int = POWER):
+    """Host-buffer multi-target estimate: complex128 frames [T, P, N] ->
+    (idx int64 [T, k], value f64 [T, k]), top-k local maxima of each map."""
+    frames = np.ascontiguousarray(frames, dtype=np.complex128)
+    if frames.ndim != 3 or frames.shape[1] != table.n_pairs or frames.shape[2] != table.scene.n_samples:
+        raise InvalidArgument("hop: frame shape mismatch")
+    T = frames.shape[0]
+    idx = np.empty((T, k), dtype=np.int64)
+    val = np.empty((T, k), dtype=np.float64)
+    _check(lib().gh_hop_estimate_topk(ctx.h, table.h, frames.ctypes.data, T, combine, k,
+                                      idx.ctypes.data, val.ctypes.data))
+    return idx, val
+
+
+def hop_estimate_topk_ptr(ctx: Context, table: HopTable, frames_ptr: int, n_trials: int,
+                          combine: int, k: int, idx_ptr: int, val_ptr: int) -> None:
+    """Raw-pointer form (pinned host buffers from the bench)."""
+    _check(lib().gh_hop_estimate_topk(ctx.h, table.h, frames_ptr, n_trials, combine, k, idx_ptr,
+                                      val_ptr))
+
+
 def campaign_hop(ctx: Context, table: HopTable, scene: Scene, trial0: int, n_trials: int,
                  combine: int = POWER, snr_db=None, out=None):
     """One Monte-Carlo step of the hop arm (src/montecarlo.cpp:140-175):
@@ -558,7 +604,7 @@ def campaign_hop(ctx: Context, table: HopTable, scene: Scene, trial0: int, n_tri
 def hop_topk(ctx: Context, table: HopTable, frames, k: int, combine: int = POWER):
     """Top-k local maxima of each trial's hop map (BASELINE c3): (idx [T,k], val [T,k])."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _table_frames(table, frames)
     T = frames.shape[0]
     idx = torch.empty((T, k), dtype=torch.int64, device=frames.device)
     val = torch.empty((T, k), dtype=torch.float32, device=frames.device)
@@ -581,11 +627,12 @@ def campaign_hop_topk(ctx: Context, table: HopTable, scene: Scene, trial0: int, 
 def topk_local_max(ctx: Context, scene: Scene, maps, k: int):
     """Top-k local maxima of caller maps fp32 [T, G] on the device."""
     torch = _torch()
+    maps = _as_maps(scene, maps)
     T = maps.shape[0]
     idx = torch.empty((T, k), dtype=torch.int64, device=maps.device)
     val = torch.empty((T, k), dtype=torch.float32, device=maps.device)
     g = scene.c_grid()
-    _check(lib().gh_topk_local_max_d(ctx.h, C.byref(g), _ptr(maps.contiguous()), T, k, _ptr(idx),
+    _check(lib().gh_topk_local_max_d(ctx.h, C.byref(g), _ptr(maps), T, k, _ptr(idx),
                                      _ptr(val)))
     return idx, val
 
@@ -593,7 +640,7 @@ def topk_local_max(ctx: Context, scene: Scene, maps, k: int):
 def location_decision_map(ctx: Context, scene: Scene, frames, combine: int = POWER):
     """location_decision_map (src/direct.cpp:90-144) for T trials: fp32 [T, G]."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _scene_frames(scene, frames)
     out = torch.empty((frames.shape[0], scene.n_bins), dtype=torch.float32, device=frames.device)
     w, g = scene.c_wave(), scene.c_grid()
     _check(lib().gh_direct_map_d(ctx.h, C.byref(w), C.byref(g), _ptr(frames), frames.shape[0],
@@ -604,7 +651,7 @@ def location_decision_map(ctx: Context, scene: Scene, frames, combine: int = POW
 def direct_argmax(ctx: Context, scene: Scene, frames, combine: int = POWER):
     """direct_estimate location stage (src/direct.cpp:230-239) batched: (idx, value)."""
     torch = _torch()
-    frames = _as_float_frames(frames)
+    frames = _scene_frames(scene, frames)
     T = frames.shape[0]
     idx = torch.empty(T, dtype=torch.int64, device=frames.device)
     val = torch.empty(T, dtype=torch.float32, device=frames.device)

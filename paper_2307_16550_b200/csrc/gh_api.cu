@@ -250,6 +250,68 @@ __global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
 }
 
 
+// Host complex128 frames [T][P][N] (the reference's FrameSet element type)
+// -> host results [T][k], pipelined over trial chunks: the H2D copy of chunk
+// i + 1 (copy stream) overlaps the conversion + estimation of chunk i
+// (context stream); each chunk's results are read back as soon as they are
+// ready. `run(d64, tc, idx_d, val_d)` estimates one chunk on the device.
+template <class Run>
+void host_frames_pipeline(gh::Ctx* c, gh::Table* t, const double* frames, int n_trials, int k,
+                          int64_t* idx, double* val, Run&& run) {
+  const int64_t per = (int64_t)t->P * t->N;
+  // ~8 chunks (>= 256 trials each): the first copy and the last chunk's
+  // compute are the exposed parts of the pipeline
+  int chunk = n_trials;
+  if (n_trials >= 2048) chunk = ((n_trials + 7) / 8 + 31) / 32 * 32;
+  const int n_chunks = (n_trials + chunk - 1) / chunk;
+  const size_t b128 = sizeof(double2) * per * chunk;
+  const int64_t nres = (int64_t)n_trials * k;
+  auto* base = static_cast<unsigned char*>(c->frames.get(
+      2 * b128 + sizeof(float2) * per * chunk + (sizeof(int64_t) + sizeof(float)) * nres));
+  double2* d128[2] = {reinterpret_cast<double2*>(base), reinterpret_cast<double2*>(base + b128)};
+  auto* d64 = reinterpret_cast<float2*>(base + 2 * b128);
+  auto* didx = reinterpret_cast<int64_t*>(d64 + per * chunk);
+  auto* dval = reinterpret_cast<float*>(didx + nres);
+  if (!c->copy_stream) GH_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->ev_ready) {
+    for (int b = 0; b < 2; ++b) {
+      GH_CUDA(cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+      GH_CUDA(cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
+    }
+    c->ev_ready = true;
+  }
+  auto* hpin = static_cast<unsigned char*>(c->host_pinned((sizeof(int64_t) + sizeof(float)) * nres));
+  auto* hidx = reinterpret_cast<int64_t*>(hpin);
+  auto* hval = reinterpret_cast<float*>(hidx + nres);
+  for (int i = 0; i < n_chunks; ++i) {
+    const int b = i & 1;
+    const int t0 = i * chunk;
+    const int tc = std::min(chunk, n_trials - t0);
+    const int64_t n = per * tc;
+    if (i >= 2) GH_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[b], 0));
+    GH_CUDA(cudaMemcpyAsync(d128[b], frames + 2 * per * t0, sizeof(double2) * n,
+                            cudaMemcpyHostToDevice, c->copy_stream));
+    GH_CUDA(cudaEventRecord(c->ev_copied[b], c->copy_stream));
+    GH_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
+    {
+      gh::KTimer kt(c, "convert");
+      k_c128_to_c64<<<blocks, 256, 0, c->stream>>>(d128[b], d64, n);
+      GH_LAUNCHED(c);
+    }
+    GH_CUDA(cudaEventRecord(c->ev_consumed[b], c->stream));
+    const int64_t r0 = (int64_t)t0 * k;
+    run(d64, tc, didx + r0, dval + r0);
+    GH_CUDA(cudaMemcpyAsync(hidx + r0, didx + r0, sizeof(int64_t) * tc * k, cudaMemcpyDeviceToHost,
+                            c->stream));
+    GH_CUDA(cudaMemcpyAsync(hval + r0, dval + r0, sizeof(float) * tc * k, cudaMemcpyDeviceToHost,
+                            c->stream));
+  }
+  GH_CUDA(cudaStreamSynchronize(c->stream));
+  std::memcpy(idx, hidx, sizeof(int64_t) * nres);
+  for (int64_t i = 0; i < nres; ++i) val[i] = hval[i];
+}
+
 // ------------------------------------------------------------ GHT1 container
 // Restates save_hop_table / load_hop_table (src/interp.cpp:225-389): the same
 // little-endian byte layout and the same runtime_error texts.
@@ -766,57 +828,29 @@ int gh_hop_estimate(gh_ctx* ctx, gh_table* table, const double* frames, int32_t 
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
     use_device(c);
-    // Pipelined over trial chunks: the H2D copy of chunk i+1 (copy stream)
-    // overlaps the conversion + FFT + gather of chunk i (context stream).
-    // Frames arrive as complex128 (the reference's FrameSet element type).
-    const int64_t per = (int64_t)t->P * t->N;
-    int chunk = n_trials;
-    if (n_trials >= 1024) chunk = ((n_trials + 3) / 4 + 31) / 32 * 32;
-    const int n_chunks = (n_trials + chunk - 1) / chunk;
-    const size_t b128 = sizeof(double2) * per * chunk;
-    auto* base = static_cast<unsigned char*>(c->frames.get(
-        2 * b128 + sizeof(float2) * per * chunk + (sizeof(int64_t) + sizeof(float)) * n_trials));
-    double2* d128[2] = {reinterpret_cast<double2*>(base), reinterpret_cast<double2*>(base + b128)};
-    auto* d64 = reinterpret_cast<float2*>(base + 2 * b128);
-    auto* didx = reinterpret_cast<int64_t*>(d64 + per * chunk);
-    auto* dval = reinterpret_cast<float*>(didx + n_trials);
-    if (!c->copy_stream) GH_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    if (!c->ev_ready) {
-      for (int b = 0; b < 2; ++b) {
-        GH_CUDA(cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
-        GH_CUDA(cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
-      }
-      c->ev_ready = true;
-    }
-    auto* hpin = static_cast<unsigned char*>(c->host_pinned((sizeof(int64_t) + sizeof(float)) * n_trials));
-    auto* hidx = reinterpret_cast<int64_t*>(hpin);
-    auto* hval = reinterpret_cast<float*>(hidx + n_trials);
-    for (int i = 0; i < n_chunks; ++i) {
-      const int b = i & 1;
-      const int t0 = i * chunk;
-      const int tc = std::min(chunk, n_trials - t0);
-      const int64_t n = per * tc;
-      if (i >= 2) GH_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[b], 0));
-      GH_CUDA(cudaMemcpyAsync(d128[b], frames + 2 * per * t0, sizeof(double2) * n,
-                              cudaMemcpyHostToDevice, c->copy_stream));
-      GH_CUDA(cudaEventRecord(c->ev_copied[b], c->copy_stream));
-      GH_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
-      const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16));
-      {
-        gh::KTimer kt(c, "convert");
-        k_c128_to_c64<<<blocks, 256, 0, c->stream>>>(d128[b], d64, n);
-        GH_LAUNCHED(c);
-      }
-      GH_CUDA(cudaEventRecord(c->ev_consumed[b], c->stream));
-      hop_argmax(c, t, d64, nullptr, tc, combine, didx + t0, dval + t0);
-      GH_CUDA(cudaMemcpyAsync(hidx + t0, didx + t0, sizeof(int64_t) * tc, cudaMemcpyDeviceToHost,
-                              c->stream));
-      GH_CUDA(cudaMemcpyAsync(hval + t0, dval + t0, sizeof(float) * tc, cudaMemcpyDeviceToHost,
-                              c->stream));
-    }
-    GH_CUDA(cudaStreamSynchronize(c->stream));
-    std::memcpy(idx, hidx, sizeof(int64_t) * n_trials);
-    for (int32_t i = 0; i < n_trials; ++i) val[i] = hval[i];
+    host_frames_pipeline(c, t, frames, n_trials, 1, idx, val,
+                         [&](const float2* d64, int tc, int64_t* di, float* dv) {
+                           hop_argmax(c, t, d64, nullptr, tc, combine, di, dv);
+                         });
+  });
+}
+
+int gh_hop_estimate_topk(gh_ctx* ctx, gh_table* table, const double* frames, int32_t n_trials,
+                         int32_t combine, int32_t k, int64_t* idx, double* val) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!frames || !idx || !val)))
+      fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (k < 1 || k > 8) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    host_frames_pipeline(c, t, frames, n_trials, k, idx, val,
+                         [&](const float2* d64, int tc, int64_t* di, float* dv) {
+                           hop_topk(c, t, d64, nullptr, tc, combine, k, di, dv);
+                         });
   });
 }
 

@@ -306,11 +306,19 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < TPL; ++i)
+          for (int i = 0; i < TPL; ++i) {
             if (vals[i] > best[i]) {
               best[i] = vals[i];
               blb[i] = (int)lb;
+            } else if (FULL && vals[i] == best[i] && a.binid &&
+                       __ldg(a.binid + entry0 + lb) < __ldg(a.binid + entry0 + blb[i])) {
+              // bank-permuted entries are not in bin order: an exact tie
+              // (zero frames, mirror-symmetric layouts) keeps the smaller
+              // bin, argmax_index's rule (src/direct.cpp:55-62); rare, so
+              // the two id loads stay off the common path
+              blb[i] = (int)lb;
             }
+          }
         }
       }
     };
@@ -330,11 +338,10 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
   }
   if constexpr (!MAPMODE) {
-    // exact ties go to the smaller bin: entry order is bin order on full
-    // plans (duplicate-row bins last) and plain tiles, not in 8-bin blocks
+    // exact ties go to the smaller bin: compare global bins (entry order is
+    // not bin order on bank-permuted full plans nor in 8-bin blocks)
     auto before = [&](int x, int y) {
-      if constexpr (FULL) return x < y;
-      else return global_bin(a, td, entry0, x) < global_bin(a, td, entry0, y);
+      return global_bin(a, td, entry0, x) < global_bin(a, td, entry0, y);
     };
     // merge the BPW lane groups of the warp (same trials, different bins)
 #pragma unroll
