@@ -314,6 +314,76 @@ int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                        const float* frames_d, int32_t n_trials, int32_t combine,
                        int64_t* idx_d, float* val_d);
 
+/* ---- multi-GPU communicator ---------------------------------------------
+ * One process per GPU. Rank 0 creates an id (ncclGetUniqueId), the caller
+ * sends it to the other ranks (e.g. torch.distributed broadcast), and every
+ * rank calls gh_comm_init with it (ncclCommInitRank) on its own context.
+ * NCCL (libnccl.so.2) is loaded at run time: without it these calls fail
+ * with GH_ERUNTIME and single-GPU campaigns still run (comm = NULL). */
+typedef struct gh_comm gh_comm;
+#define GH_COMM_ID_BYTES 128
+int gh_comm_unique_id(uint8_t id[GH_COMM_ID_BYTES]);
+int gh_comm_init(gh_ctx* ctx, const uint8_t id[GH_COMM_ID_BYTES], int32_t n_ranks, int32_t rank,
+                 gh_comm** out);
+int gh_comm_info(const gh_comm* comm, int32_t* n_ranks, int32_t* rank);
+int gh_comm_destroy(gh_comm* comm);
+
+/* ---- Monte-Carlo campaign driver ----------------------------------------
+ * run_monte_carlo (src/montecarlo.cpp:99-179) on the device: for every
+ * density (one hop table each, built on the device; LocationGrid::build's
+ * axis count at spacing / density over the grid's extent, model.cpp:91-105),
+ * every SNR and every algorithm, the campaign's n_trials trials — sharded
+ * over the communicator's ranks in contiguous blocks, each trial keyed by
+ * (seed, global trial) so estimates do not depend on the rank count — run
+ * synthesis, the estimator and the statistics on the device. A trial's
+ * estimates (topk per trial: argmax or the k best local maxima) are assigned
+ * to its targets by the permutation of least total squared distance; the
+ * cell counts hits per threshold (hit_ratio, montecarlo.cpp:181-190), the
+ * squared-error sum (RMSE) and half-resolution hits. Cell vectors are summed
+ * over ranks with one NCCL all-reduce. Optional CSVs follow write_trial_csv /
+ * write_summary_csv (montecarlo.cpp:230-284; one trial row per target, v =
+ * 0 as the campaign has no slow-time axis; written by rank 0).
+ * Algorithm ids follow the reference's enum order (scenario.hpp:12). */
+enum gh_algorithm { GH_ALGO_INDIRECT = 0, GH_ALGO_DIRECT = 1, GH_ALGO_HOP = 2 };
+#define GH_MAX_THRESHOLDS 32
+typedef struct {
+  gh_wave wave;               /* waveform + TX-RX pairs                      */
+  gh_grid grid;               /* location grid at density 1                  */
+  gh_campaign scene;          /* truth / amplitude / SNR model               */
+  int32_t scheme;             /* hop table interpolation scheme              */
+  int32_t wrap;               /* 0: the reference's window checks           */
+  int32_t combine;            /* GH_POWER / GH_MAGNITUDE                     */
+  int32_t n_algorithms;
+  const int32_t* algorithms;  /* gh_algorithm values, in record order        */
+  int32_t n_snr;              /* 0: the scene's own SNR model, one cell      */
+  const double* snr_db;       /* per-cell SNR (fixed mode); NaN = noiseless  */
+  int32_t n_density;          /* 0: density 1                                */
+  const double* density;
+  int32_t n_thresholds;       /* 0: 0.2, 0.4 .. 3.0 m (scenario.cpp:177-179) */
+  const double* thresholds_m;
+  int64_t n_trials;           /* per cell, whole job                         */
+  int32_t topk;               /* estimates per trial (<= 6 for statistics)   */
+  int32_t batch;              /* trials per device batch, 0: automatic       */
+  const char* trial_csv;      /* nullable                                    */
+  const char* summary_csv;    /* nullable                                    */
+} gh_campaign_desc;
+typedef struct {
+  int32_t algorithm, density_idx, snr_idx, n_thresholds;
+  double density, snr_db;     /* snr_db NaN: noiseless / per-pair model      */
+  int64_t trials;             /* trials of the cell (all ranks)              */
+  int64_t estimates;          /* scored (trial, target) pairs                */
+  double thresholds_m[GH_MAX_THRESHOLDS];
+  double hits[GH_MAX_THRESHOLDS];
+  double hit_ratio[GH_MAX_THRESHOLDS];
+  double hits_half_res;       /* within half a range resolution c / (4 B)    */
+  double sq_err_sum, err_sum, rmse_m;
+  double online_ms;           /* device time of the estimator, max over ranks */
+  double offline_ms;          /* hop table build of the density (hop cells)  */
+  double mean_online_ns;      /* online_ms per trial of the largest shard    */
+} gh_cell_stats;
+int gh_campaign_run(gh_ctx* ctx, gh_comm* comm, const gh_campaign_desc* desc, gh_cell_stats* out,
+                    int32_t capacity, int32_t* n_cells);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,8 @@ from .api import (Context, HopTable, InvalidArgument, GridhopRuntimeError, Domai
                   location_decision_map, direct_argmax, argmax_index, lib, exported_symbols,
                   scene_hash, ght1_write, ght1_read, table_save, table_load,
                   indirect_argmin, multilaterate, hop_map_mc, hop_argmax_mc, mrf1_write,
-                  mrf1_read, velocity_grid, velocity)
+                  mrf1_read, velocity_grid, velocity, hop_estimate_topk, campaign_run, Comm,
+                  comm_unique_id)
 
 __all__ = [
     "scene", "Scene", "baseline", "small", "Context", "HopTable", "InvalidArgument",
@@ -25,5 +26,5 @@ __all__ = [
     "lib", "exported_symbols", "precompute_hop_table_shard", "hop_topk", "campaign_hop_topk",
     "topk_local_max", "scene_hash", "ght1_write", "ght1_read", "table_save", "table_load",
     "indirect_argmin", "multilaterate", "hop_map_mc", "hop_argmax_mc", "mrf1_write", "mrf1_read",
-    "velocity_grid", "velocity",
+    "velocity_grid", "velocity", "hop_estimate_topk", "campaign_run", "Comm", "comm_unique_id",
 ]

@@ -77,6 +77,35 @@ class Ght1Header(C.Structure):
                 ("os_range", C.c_int32), ("n_samples", C.c_int32), ("scene_hash", C.c_uint64),
                 ("max_residual", C.c_double)]
 
+MAX_THRESHOLDS = 32
+ALGO_INDIRECT, ALGO_DIRECT, ALGO_HOP = 0, 1, 2  # Algorithm (scenario.hpp:12)
+ALGO_IDS = {"indirect": ALGO_INDIRECT, "direct": ALGO_DIRECT, "hop": ALGO_HOP}
+
+
+class CampaignDesc(C.Structure):
+    """gh_campaign_desc: a Scenario (scenario.hpp:22-52) for the device driver."""
+    _fields_ = [("wave", CWave), ("grid", CGrid), ("scene", CCampaign), ("scheme", C.c_int32),
+                ("wrap", C.c_int32), ("combine", C.c_int32), ("n_algorithms", C.c_int32),
+                ("algorithms", C.POINTER(C.c_int32)), ("n_snr", C.c_int32),
+                ("snr_db", C.POINTER(C.c_double)), ("n_density", C.c_int32),
+                ("density", C.POINTER(C.c_double)), ("n_thresholds", C.c_int32),
+                ("thresholds_m", C.POINTER(C.c_double)), ("n_trials", C.c_int64),
+                ("topk", C.c_int32), ("batch", C.c_int32), ("trial_csv", C.c_char_p),
+                ("summary_csv", C.c_char_p)]
+
+
+class CellStats(C.Structure):
+    """gh_cell_stats: one (density, SNR, algorithm) cell of a campaign."""
+    _fields_ = [("algorithm", C.c_int32), ("density_idx", C.c_int32), ("snr_idx", C.c_int32),
+                ("n_thresholds", C.c_int32), ("density", C.c_double), ("snr_db", C.c_double),
+                ("trials", C.c_int64), ("estimates", C.c_int64),
+                ("thresholds_m", C.c_double * MAX_THRESHOLDS),
+                ("hits", C.c_double * MAX_THRESHOLDS), ("hit_ratio", C.c_double * MAX_THRESHOLDS),
+                ("hits_half_res", C.c_double), ("sq_err_sum", C.c_double), ("err_sum", C.c_double),
+                ("rmse_m", C.c_double), ("online_ms", C.c_double), ("offline_ms", C.c_double),
+                ("mean_online_ns", C.c_double)]
+
+
 _lib = None
 
 
@@ -140,6 +169,11 @@ def lib() -> C.CDLL:
             "gh_ght1_write": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp]),
             "gh_ght1_read": (C.c_int, [C.c_char_p, P(Ght1Header), vp, vp, i64]),
             "gh_table_save": (C.c_int, [vp, C.c_char_p, u64]),
+            "gh_comm_unique_id": (C.c_int, [vp]),
+            "gh_comm_init": (C.c_int, [vp, vp, i32, i32, P(vp)]),
+            "gh_comm_info": (C.c_int, [vp, P(i32), P(i32)]),
+            "gh_comm_destroy": (C.c_int, [vp]),
+            "gh_campaign_run": (C.c_int, [vp, vp, P(CampaignDesc), P(CellStats), i32, P(i32)]),
             "gh_table_load": (C.c_int, [vp, C.c_char_p, P(CWave), P(CGrid), u64, P(vp)]),
         }
         for name, (res, args) in sig.items():
@@ -667,3 +701,101 @@ def argmax_index(values) -> int:
     if v.size == 0:
         raise InvalidArgument("argmax of empty scan")
     return int(np.argmax(v))  # numpy returns the first occurrence of the max
+
+
+# ---------------------------------------------------------------- multi-GPU + campaigns
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId on this rank (rank 0), to broadcast to the others."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().gh_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Comm:
+    """gh_comm: one NCCL communicator rank on `ctx`'s device (one process
+    per GPU). `uid` comes from comm_unique_id() on rank 0."""
+
+    def __init__(self, ctx: Context, uid: bytes, n_ranks: int, rank: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(lib().gh_comm_init(ctx.h, buf, n_ranks, rank, C.byref(h)))
+        self.h, self.n_ranks, self.rank = h, n_ranks, rank
+
+    @classmethod
+    def from_torch_distributed(cls, ctx: Context) -> "Comm":
+        """Rank 0's id broadcast over the initialised torch.distributed group."""
+        import torch.distributed as dist
+        obj = [comm_unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(ctx, obj[0], dist.get_world_size(), dist.get_rank())
+
+    def close(self) -> None:
+        if self.h:
+            _check(lib().gh_comm_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def campaign_run(ctx: Context, scene: Scene, n_trials: int | None = None, algorithms=("hop",),
+                 snr_db=None, densities=None, thresholds=None, topk: int | None = None,
+                 comm: Comm | None = None, batch: int = 0, trial_csv=None, summary_csv=None,
+                 scheme: int | None = None, wrap: bool | None = None, combine: int = POWER):
+    """run_monte_carlo (src/montecarlo.cpp:99-179) on the device: every
+    (density, SNR, algorithm) cell over n_trials trials (sharded over
+    `comm`'s ranks), statistics on the device, one NCCL all-reduce per cell.
+    snr_db: None = the scene's SNR model (one cell), else a list (NaN =
+    noiseless). Returns one dict per cell (record order density, SNR,
+    algorithm) with hit ratios per threshold, RMSE, half-resolution hits and
+    the device times."""
+    algos = [ALGO_IDS[a] if isinstance(a, str) else int(a) for a in algorithms]
+    alg_arr = (C.c_int32 * len(algos))(*algos)
+    d = CampaignDesc()
+    d.wave = scene.c_wave()
+    d.grid = scene.c_grid()
+    d.scene = scene.c_campaign()
+    d.scheme = scene.scheme if scheme is None else scheme
+    d.wrap = int(scene.wrap if wrap is None else wrap)
+    d.combine = combine
+    d.n_algorithms = len(algos)
+    d.algorithms = alg_arr
+    keep = [alg_arr]
+    if snr_db is not None:
+        arr = (C.c_double * len(snr_db))(*[float(x) for x in snr_db])
+        keep.append(arr)
+        d.n_snr, d.snr_db = len(snr_db), arr
+    if densities is not None:
+        arr = (C.c_double * len(densities))(*[float(x) for x in densities])
+        keep.append(arr)
+        d.n_density, d.density = len(densities), arr
+    if thresholds is not None:
+        arr = (C.c_double * len(thresholds))(*[float(x) for x in thresholds])
+        keep.append(arr)
+        d.n_thresholds, d.thresholds_m = len(thresholds), arr
+    d.n_trials = int(n_trials or scene.trials)
+    d.topk = int(topk or scene.topk)
+    d.batch = int(batch)
+    d.trial_csv = str(trial_csv).encode() if trial_csv else None
+    d.summary_csv = str(summary_csv).encode() if summary_csv else None
+    n_cells = max(1, len(densities or [1])) * max(1, len(snr_db or [0])) * len(algos)
+    out = (CellStats * n_cells)()
+    got = C.c_int32()
+    _check(lib().gh_campaign_run(ctx.h, comm.h if comm else None, C.byref(d), out, n_cells,
+                                 C.byref(got)))
+    names = {v: k for k, v in ALGO_IDS.items()}
+    cells = []
+    for cs in out[:got.value]:
+        nth = cs.n_thresholds
+        cells.append({
+            "algorithm": names[cs.algorithm], "density": cs.density, "snr_db": cs.snr_db,
+            "trials": cs.trials, "estimates": cs.estimates,
+            "thresholds_m": list(cs.thresholds_m[:nth]), "hits": list(cs.hits[:nth]),
+            "hit_ratio": list(cs.hit_ratio[:nth]), "hits_half_res": cs.hits_half_res,
+            "sq_err_sum": cs.sq_err_sum, "err_sum": cs.err_sum, "rmse_m": cs.rmse_m,
+            "online_ms": cs.online_ms, "offline_ms": cs.offline_ms,
+            "mean_online_ns": cs.mean_online_ns})
+    return cells

@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libgridhop_b200.so"
 SOURCES = ["gh_api.cu", "gh_fft.cu", "gh_table.cu", "gh_gather.cu", "gh_direct.cu",
            "gh_direct_umma.cu", "gh_peaks.cu", "gh_topk.cu", "gh_indirect.cu",
-           "gh_velocity.cu"]
+           "gh_velocity.cu", "gh_campaign.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -70,7 +70,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed for {failed}")
     if force or _stale(LIB, objs):
         cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-               *map(str, objs), "-o", str(LIB), "-lcudart"]
+               *map(str, objs), "-o", str(LIB), "-lcudart", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

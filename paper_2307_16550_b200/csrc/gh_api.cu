@@ -111,7 +111,7 @@ void free_table(gh::Table* t) {
   cudaFree(t->txrx_d);
   cudaFree(t->idx_d);
   cudaFree(t->coef_d);
-  for (gh::Plan* pl : {&t->plan, &t->plan_map}) {
+  for (gh::Plan* pl : {&t->plan, &t->plan_map, &t->plan_topk}) {
     cudaFree(pl->tiles_d);
     cudaFree(pl->win_d);
     cudaFree(pl->rows_d);
@@ -167,6 +167,33 @@ gh::SynthParams make_synth(gh::Ctx* c, const double* txrx_d, double scale, const
   return sp;
 }
 
+// Campaign synthesis (asynchronous calls): window / geometry violations
+// accumulate in a persistent device flag that the next synchronising call
+// (gh_ctx_synchronize, gh_campaign_run) reports and clears, so the hot path
+// needs no per-step sync (synth.cpp:27-29, model.cpp:50 error texts).
+gh::SynthParams make_campaign_synth(gh::Ctx* c, gh::Table* t, const gh_campaign* camp,
+                                    uint64_t trial0) {
+  gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, t->wrap);
+  if (!c->synth_flag_d) {
+    c->synth_flag_d = static_cast<int*>(c->flagbuf.get(sizeof(int)));
+    GH_CUDA(cudaMemsetAsync(c->synth_flag_d, 0, sizeof(int), c->stream));
+  }
+  sp.err_flag_d = c->synth_flag_d;
+  c->synth_pending = true;
+  return sp;
+}
+
+void check_deferred_synth(gh::Ctx* c) {
+  if (!c->synth_pending) return;
+  int h = 0;
+  GH_CUDA(cudaMemcpyAsync(&h, c->synth_flag_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  GH_CUDA(cudaMemsetAsync(c->synth_flag_d, 0, sizeof(int), c->stream));
+  GH_CUDA(cudaStreamSynchronize(c->stream));
+  c->synth_pending = false;
+  if (h & 2) fail(GH_EDOMAIN, "degenerate geometry: target coincides with a station");
+  if (h & 1) fail(GH_ERUNTIME, "scene outside unambiguous window");
+}
+
 void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
   int h = 0;
   GH_CUDA(cudaMemcpyAsync(&h, sp.err_flag_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -180,6 +207,41 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
 // gather launches fill the GPU), then k_topk_localmax picks the peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
+  if (gh::Plan* tp = gh::build_plan_topk(c, t)) {
+    // fused: the gather keeps each tile's values in shared memory and picks
+    // the tile's local maxima there; per (trial, tile) K keys, then a merge.
+    // Trial chunks bound the spectra (~4 GB) and candidate (~1 GB) scratch.
+    const int tb = tp->tb;
+    const int64_t n_lists = (int64_t)tp->n_tiles * K;
+    const int64_t spec_per_trial = (int64_t)t->P * t->M * tp->esize;
+    int64_t chunk = std::min<int64_t>((int64_t(1) << 32) / spec_per_trial,
+                                      (int64_t(1) << 30) / (n_lists * 8));
+    chunk = std::max<int64_t>(tb, chunk / tb * tb);
+    chunk = std::min<int64_t>(chunk, (T + tb - 1) / tb * tb);
+    auto* cand = static_cast<unsigned long long*>(
+        c->mapbuf.get(sizeof(unsigned long long) * (chunk * n_lists + chunk)));
+    unsigned long long* thr = cand + chunk * n_lists;
+    for (int t0 = 0; t0 < T; t0 += static_cast<int>(chunk)) {
+      const int tc = static_cast<int>(std::min<int64_t>(chunk, T - t0));
+      gh::SynthParams sc{};
+      const gh::SynthParams* spc = nullptr;
+      if (sp) {
+        sc = *sp;
+        sc.trial0 += static_cast<uint64_t>(t0);
+        spc = &sc;
+      }
+      const float2* fr = frames ? frames + (int64_t)t0 * t->P * t->N : nullptr;
+      const size_t bytes = static_cast<size_t>((tc + tb - 1) / tb) * t->P * t->M * tb * tp->esize;
+      void* spec = c->spectra.get(bytes);
+      gh::launch_fft(c, fr, spc, tc, t->P, t->N, t->os, tb,
+                     combine == GH_MAGNITUDE ? gh::FFT_GATHER_MAG : gh::FFT_GATHER_POWER, spec);
+      GH_CUDA(cudaMemsetAsync(thr, 0, sizeof(unsigned long long) * tc, c->stream));
+      gh::launch_gather_topk(c, t, spec, tc, K, cand, thr);
+      gh::launch_topk_merge(c, cand, tc, static_cast<int>(n_lists), K, idx_d + (int64_t)t0 * K,
+                            val_d + (int64_t)t0 * K);
+    }
+    return;
+  }
   const int tb = gh::build_plan(c, t, true).tb;
   int64_t chunk = (int64_t(1) << 31) / std::max<int64_t>(t->G, 1);
   chunk = std::max<int64_t>(tb, chunk / tb * tb);
@@ -473,6 +535,29 @@ struct Fnv1a {
 
 }  // namespace
 
+namespace gh {
+// Operations shared with the campaign driver (gh_campaign.cu).
+void op_check_wave(const gh_wave* w) { check_wave(w); }
+int64_t op_grid_size(const gh_grid* g) { return grid_size(g); }
+void op_hop_argmax(Ctx* c, Table* t, const float2* frames, const SynthParams* sp, int T,
+                   int combine, int64_t* idx_d, float* val_d) {
+  hop_argmax(c, t, frames, sp, T, combine, idx_d, val_d);
+}
+void op_hop_topk(Ctx* c, Table* t, const float2* frames, const SynthParams* sp, int T, int combine,
+                 int K, int64_t* idx_d, float* val_d) {
+  hop_topk(c, t, frames, sp, T, combine, K, idx_d, val_d);
+}
+SynthParams op_make_synth(Ctx* c, const double* txrx_d, double scale, const gh_campaign* camp,
+                          uint64_t trial0, int wrap) {
+  return make_synth(c, txrx_d, scale, camp, trial0, wrap);
+}
+void op_check_synth(Ctx* c, const SynthParams& sp) { check_synth_flag(c, sp); }
+Table* op_new_table(Ctx* c, const gh_wave* w, const gh_grid* g, int scheme) {
+  return new_table(c, w, g, scheme);
+}
+void op_free_table(Table* t) { free_table(t); }
+}  // namespace gh
+
 extern "C" {
 
 const char* gh_last_error(void) { return g_err.c_str(); }
@@ -513,6 +598,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->seeds.release();
     c->amax.release();
     c->misc2.release();
+    c->flagbuf.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)
@@ -555,6 +641,7 @@ int gh_ctx_synchronize(gh_ctx* ctx) {
     if (!c) fail(GH_EINVAL, "ctx: null argument");
     use_device(c);
     GH_CUDA(cudaStreamSynchronize(c->stream));
+    check_deferred_synth(c);
   });
 }
 
@@ -641,6 +728,7 @@ int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, int32_
     use_device(c);
     gh::Table* t = new_table(c, wave, grid, scheme);
     try {
+      t->wrap = wrap ? 1 : 0;
       gh::build_table_device(c, t, wrap);
       gh::build_plan(c, t);
     } catch (...) {
@@ -669,6 +757,7 @@ int gh_table_build_shard(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, 
     t->bin0 = layer_lo * layer;
     t->G = (int64_t)(layer_hi - layer_lo) * layer;
     try {
+      t->wrap = wrap ? 1 : 0;
       gh::build_table_device(c, t, wrap);
       gh::build_plan(c, t);
     } catch (...) {
@@ -865,8 +954,9 @@ int gh_campaign_hop_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp, uin
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
     use_device(c);
-    // wrap mode always: the table was built against the same scene
-    const gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, 1);
+    // the table's window policy (wrap = 0: the reference's window check,
+    // reported by the next synchronising call)
+    const gh::SynthParams sp = make_campaign_synth(c, t, camp, trial0);
     hop_argmax(c, t, nullptr, &sp, n_trials, combine, idx_d, val_d);
   });
 }
@@ -901,7 +991,7 @@ int gh_campaign_hop_topk_d(gh_ctx* ctx, gh_table* table, const gh_campaign* camp
     if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
     if (n_trials == 0) return;
     use_device(c);
-    const gh::SynthParams sp = make_synth(c, t->txrx_d, t->scale, camp, trial0, 1);
+    const gh::SynthParams sp = make_campaign_synth(c, t, camp, trial0);
     hop_topk(c, t, nullptr, &sp, n_trials, combine, k, idx_d, val_d);
   });
 }
@@ -1255,6 +1345,51 @@ int gh_direct_velocity_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                          int64_t* vidx_d, float* vval_d) {
   return velocity_entry(ctx, wave, grid, vgrid, frames_d, n_trials, n_chirps, loc_d, vidx_d,
                         vval_d, false);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int gh_comm_unique_id(uint8_t id[GH_COMM_ID_BYTES]) {
+  return guarded([&] {
+    if (!id) fail(GH_EINVAL, "comm: null argument");
+    gh::comm_unique_id(id);
+  });
+}
+
+int gh_comm_init(gh_ctx* ctx, const uint8_t id[GH_COMM_ID_BYTES], int32_t n_ranks, int32_t rank,
+                 gh_comm** out) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || !id || !out) fail(GH_EINVAL, "comm: null argument");
+    use_device(c);
+    *out = reinterpret_cast<gh_comm*>(gh::comm_init(c, id, n_ranks, rank));
+  });
+}
+
+int gh_comm_info(const gh_comm* comm, int32_t* n_ranks, int32_t* rank) {
+  return guarded([&] {
+    if (!comm || !n_ranks || !rank) fail(GH_EINVAL, "comm: null argument");
+    int n = 0, r = 0;
+    gh::comm_info(reinterpret_cast<const gh::Comm*>(comm), &n, &r);
+    *n_ranks = n;
+    *rank = r;
+  });
+}
+
+int gh_comm_destroy(gh_comm* comm) {
+  return guarded([&] { gh::comm_destroy(reinterpret_cast<gh::Comm*>(comm)); });
+}
+
+int gh_campaign_run(gh_ctx* ctx, gh_comm* comm, const gh_campaign_desc* desc, gh_cell_stats* out,
+                    int32_t capacity, int32_t* n_cells) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "campaign: null argument");
+    use_device(c);
+    gh::campaign_run(c, reinterpret_cast<gh::Comm*>(comm), desc, out, capacity, n_cells);
+  });
 }
 
 }  // extern "C"

@@ -61,7 +61,7 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2, flagbuf;
   int twiddle_m = 0;
   int direct_impl = 0;  // 0: tcgen05 3xFP16, 1: CUDA-core fp32, 2: tcgen05 v1, 3: tcgen05 3xTF32
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
@@ -89,6 +89,9 @@ struct Ctx {
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   std::vector<std::pair<std::string, KernelTimes>> times;
+  // deferred campaign-synthesis error flag (window / degenerate geometry)
+  int* synth_flag_d = nullptr;
+  bool synth_pending = false;
 };
 
 // Records events around one launch when ctx->timing is set.
@@ -130,7 +133,16 @@ struct TileDesc {
   int32_t rows;       // staged rows in total (sum over pairs)
   int32_t blk;        // 0: plain order; else 1 + log2 of the 8-bin block's (x, y, z)
                       // extents at bits 0-1, 2-3, 4-5 (extents divide wx, wy, wz)
+  // top-K plans: the box above is the tile's core box grown by a 1-bin
+  // halo (clipped to the grid); the core (the bins this tile reports) is
+  // [c*0, c*0 + cw*) inside it. Other plans: core = box.
+  int32_t cx0, cy0, cz0, cwx, cwy, cwz;
 };
+
+// values buffer pitch (bins) of a top-K tile row: == 2 mod 4, so the 32-byte
+// rows of a 2 x 4 block's upper and lower bin pairs fall in opposite halves of
+// the shared-memory banks
+__host__ __device__ __forceinline__ int topk_pitch(int wx) { return wx + ((6 - wx % 4) % 4); }
 
 // Local entry lb of a tile -> tile coordinates. Plain tiles run x-fastest;
 // blocked tiles (8-trial power argmax plans) run 8-bin blocks (2 x 4 x 1 on
@@ -172,6 +184,10 @@ struct Plan {
   uint32_t* crow_d = nullptr;    // [entries] compact ring rows (cbits per pair), or null
   int cbits = 0;
   int64_t n_entries = 0;
+  // top-K plans (halo tiles): per-tile values buffer in shared memory
+  bool halo = false;
+  size_t vals_bytes = 0;   // the largest tile's [pitch * wy * wz][tb] fp32 values
+  int pick_blocks = 0;     // the largest tile's 4 x 4 core blocks (prune seeds)
 };
 
 struct Table {
@@ -190,6 +206,9 @@ struct Table {
   double max_residual = 0.0;
   Plan plan;      // argmax gathers (tiled power plans: 8-bin blocked entries)
   Plan plan_map;  // map-mode gathers (plain x-fastest entries: contiguous map stores)
+  Plan plan_topk; // fused top-K gathers (halo tiles, values kept in shared memory)
+  bool topk_fused_ok = true;  // false once the plan builder found no fused tiling
+  int wrap = 1;   // the window policy the table was built with (campaign synthesis)
 };
 
 // ------------------------------------------------------------ device helpers
@@ -255,6 +274,15 @@ void build_table_device(Ctx* ctx, Table* t, int wrap);
 // the gather plan of a table for argmax (mapmode = false) or map-writing
 // gathers, built on first use
 Plan& build_plan(Ctx* ctx, Table* t, bool mapmode = false);
+// the fused top-K plan (2-D K = 1 tiled tables): nullptr when the table does
+// not admit one (full-ring / K = 3 / 3-D / shard tables use map + pick)
+Plan* build_plan_topk(Ctx* ctx, Table* t);
+// fused gather + top-K local maxima: per (trial, tile) candidate keys into
+// cand_d [T][n_tiles][K] (thr_d [T] zeroed by the caller), then the merge
+void launch_gather_topk(Ctx* ctx, Table* t, const void* spec_d, int T, int K,
+                        unsigned long long* cand_d, unsigned long long* thr_d);
+void launch_topk_merge(Ctx* ctx, const unsigned long long* cand_d, int T, int n_lists, int K,
+                       int64_t* idx_d, float* val_d);
 void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
                    float* map_d, unsigned long long* keys_d);
 void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
@@ -271,6 +299,27 @@ void launch_range_peaks(Ctx* ctx, const float2* spec_d, int64_t rows, int M, int
                         double* rhat_d);
 void launch_multilaterate(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                           const double* rhat_d, int T, int64_t* idx_d, double* res_d);
+// multi-GPU communicator (NCCL, loaded at run time) and the campaign driver
+// (gh_campaign.cu)
+struct Comm;
+void comm_unique_id(uint8_t* id);
+Comm* comm_init(Ctx* c, const uint8_t* id, int n_ranks, int rank);
+void comm_destroy(Comm* cm);
+void comm_info(const Comm* cm, int* n_ranks, int* rank);
+void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* out,
+                  int32_t capacity, int32_t* n_cells);
+// host operations of gh_api.cu used by the campaign driver (gh_campaign.cu)
+void op_check_wave(const gh_wave* w);
+int64_t op_grid_size(const gh_grid* g);
+void op_hop_argmax(Ctx* c, Table* t, const float2* frames, const SynthParams* sp, int T,
+                   int combine, int64_t* idx_d, float* val_d);
+void op_hop_topk(Ctx* c, Table* t, const float2* frames, const SynthParams* sp, int T, int combine,
+                 int K, int64_t* idx_d, float* val_d);
+SynthParams op_make_synth(Ctx* c, const double* txrx_d, double scale, const gh_campaign* camp,
+                          uint64_t trial0, int wrap);
+void op_check_synth(Ctx* c, const SynthParams& sp);
+Table* op_new_table(Ctx* c, const gh_wave* w, const gh_grid* g, int scheme);
+void op_free_table(Table* t);
 void direct_map_simt(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const float2* frames_d, int T, int combine, float* map_d,
                      unsigned long long* keys_d);

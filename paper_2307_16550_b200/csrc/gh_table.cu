@@ -652,6 +652,9 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
                              td.wz % bext[2] == 0
                          ? blk_code
                          : 0;
+            td.cwx = td.wx;
+            td.cwy = td.wy;
+            td.cwz = td.wz;
             off += (int64_t)td.wx * td.wy * td.wz;
             tl.tiles.push_back(td);
           }
@@ -784,6 +787,201 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
   if (pl.full && !pl.k3 && P <= 8) permute_for_banks(ctx, t, pl);
   pl.built = true;
   return pl;
+}
+
+
+// ---------------------------------------------------------------- top-K plan
+
+// Fused top-K plans (BASELINE c3: 2-D grid, K = 1, many pairs): 8-trial
+// batches as the argmax plan, but each tile's core box is grown by a 1-bin
+// halo so the gather itself evaluates every neighbour a core bin's
+// local-maximum test needs; the tile's values for its 8 trials then stay in
+// shared memory next to the range windows (gh_gather.cu k_gather_topk).
+// Windows + values must share one CTA's shared memory, so tiles are smaller
+// than the argmax plan's (~56 x 56 bins on c3 instead of ~113 x 113).
+constexpr size_t kTopkSmem = 224 * 1024;  // windows + values + per-warp lists
+constexpr size_t kTopkLists = 24 * 8 * 8 * sizeof(unsigned long long);
+// the pick region first holds each trial's verified 4 x 4 block maxima
+inline size_t topk_pick_bytes(int blocks) {
+  return std::max<size_t>(kTopkLists, (size_t)8 * blocks * sizeof(unsigned long long));
+}
+
+Plan* build_plan_topk(Ctx* ctx, Table* t) {
+  Plan& pl = t->plan_topk;
+  if (pl.built) return &pl;
+  if (!t->topk_fused_ok) return nullptr;
+  const gh_grid& g = t->grid;
+  const int P = t->P, M = t->M;
+  const size_t full_bytes = static_cast<size_t>(P) * M * 16 * 4;
+  const bool full_ring = full_bytes <= kStageBudget && M <= 65535 / P;
+  if (t->K != 1 || g.n[2] > 1 || full_ring || t->bin0 != 0 ||
+      t->G != (int64_t)g.n[0] * g.n[1] || P > 64) {
+    t->topk_fused_ok = false;
+    return nullptr;
+  }
+  pl.full = false;
+  pl.k3 = 0;
+  pl.esize = 4;
+  pl.tb = 8;
+  pl.p4 = (P + 3) / 4 * 4;
+  pl.chunk_pairs = pl.p4;
+  pl.halo = true;
+  struct Tiling {
+    std::vector<TileDesc> tiles;
+    std::vector<int4> win;
+    int max_rows = 0;
+    int64_t entries = 0;
+    size_t vals = 0;
+    int blocks = 0;
+  };
+  int2* mm_d = nullptr;
+  TileDesc* tiles_d = nullptr;
+  size_t mm_cap = 0, tiles_cap = 0;
+  // core widths: x even, y == 2 mod 4, so interior halo boxes (core + 2)
+  // are whole 2 x 4 blocks and run in the blocked entry order
+  auto try_tiling = [&](int w) {
+    Tiling tl;
+    const int cw_x = std::max(2, w - w % 2);
+    const int cw_y = std::max(2, w - ((w - 2) % 4 + 4) % 4);
+    int64_t off = 0;
+    for (int y = 0; y < g.n[1]; y += cw_y)
+      for (int x = 0; x < g.n[0]; x += cw_x) {
+        TileDesc td{};
+        const int ex0 = std::max(0, x - 1), ey0 = std::max(0, y - 1);
+        const int ex1 = std::min(g.n[0], x + cw_x + 1), ey1 = std::min(g.n[1], y + cw_y + 1);
+        td.x0 = ex0;
+        td.y0 = ey0;
+        td.z0 = 0;
+        td.wx = ex1 - ex0;
+        td.wy = ey1 - ey0;
+        td.wz = 1;
+        td.cx0 = x - ex0;
+        td.cy0 = y - ey0;
+        td.cz0 = 0;
+        td.cwx = std::min(cw_x, g.n[0] - x);
+        td.cwy = std::min(cw_y, g.n[1] - y);
+        td.cwz = 1;
+        td.entry_off = off;
+        td.blk = td.wx % 2 == 0 && td.wy % 4 == 0 ? 1 + 1 + (2 << 2) : 0;  // 2 x 4 x 1
+        off += (int64_t)td.wx * td.wy;
+        tl.vals = std::max(tl.vals, (size_t)topk_pitch(td.wx) * td.wy * 8 * sizeof(float));
+        tl.blocks = std::max(tl.blocks, ((td.cwx + 3) / 4) * ((td.cwy + 3) / 4));
+        tl.tiles.push_back(td);
+      }
+    tl.entries = off;
+    const size_t nt = tl.tiles.size();
+    if (nt > tiles_cap) {
+      if (tiles_d) cudaFree(tiles_d);
+      GH_CUDA(cudaMalloc(&tiles_d, sizeof(TileDesc) * nt));
+      tiles_cap = nt;
+    }
+    if (nt * P > mm_cap) {
+      if (mm_d) cudaFree(mm_d);
+      GH_CUDA(cudaMalloc(&mm_d, sizeof(int2) * nt * P));
+      mm_cap = nt * P;
+    }
+    GH_CUDA(cudaMemcpyAsync(tiles_d, tl.tiles.data(), sizeof(TileDesc) * nt,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    k_tile_minmax<<<static_cast<int>(nt), 256, 0, ctx->stream>>>(tiles_d, g, t->txrx_d, t->scale,
+                                                                 t->os, P, mm_d);
+    GH_LAUNCHED(ctx);
+    std::vector<int2> mm(nt * P);
+    GH_CUDA(cudaMemcpyAsync(mm.data(), mm_d, sizeof(int2) * mm.size(), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    GH_CUDA(cudaStreamSynchronize(ctx->stream));
+    tl.win.assign(mm.size(), make_int4(0, 0, 0, 0));
+    for (size_t ti = 0; ti < nt; ++ti) {
+      int rs = 0;
+      for (int p = 0; p < P; ++p) {
+        const int2 m = mm[ti * P + p];
+        int base = m.x - 2, len = m.y - m.x + 5;
+        if (len >= M) {
+          base = 0;
+          len = M;
+        }
+        base = ((base % M) + M) % M;
+        tl.win[ti * P + p] = make_int4(base, len, rs, 0);
+        rs += len;
+      }
+      tl.tiles[ti].rows = rs;
+      tl.max_rows = std::max(tl.max_rows, rs);
+    }
+    return tl;
+  };
+  auto smem_of = [&](const Tiling& tl) {
+    return ((size_t)tl.max_rows * 8 * 4 + 127) / 128 * 128 + (tl.vals + 127) / 128 * 128 +
+           topk_pick_bytes(tl.blocks);
+  };
+  auto fits = [&](const Tiling& tl) {
+    return smem_of(tl) <= kTopkSmem && tl.max_rows * 2 <= 65535;  // 16-byte units, L = 2
+  };
+  // start near values ~ 45 % of the budget, then shrink / grow the core
+  int w = static_cast<int>(std::sqrt(0.45 * kTopkSmem / 32.0)) - 3;
+  w = std::max(4, std::min(w, std::max(g.n[0], g.n[1])));
+  Tiling best = try_tiling(w);
+  for (int i = 0; i < 40 && !fits(best) && w > 4; ++i) {
+    w = std::max(4, w * 9 / 10);
+    best = try_tiling(w);
+  }
+  if (!fits(best)) {
+    cudaFree(tiles_d);
+    cudaFree(mm_d);
+    t->topk_fused_ok = false;
+    return nullptr;
+  }
+  for (int i = 0; i < 32; ++i) {
+    if (w >= std::max(g.n[0], g.n[1])) break;
+    Tiling bigger = try_tiling(w + 4);
+    if (!fits(bigger)) break;
+    best = std::move(bigger);
+    w += 4;
+  }
+  cudaFree(mm_d);
+  // final tiles (the scratch holds the last tried tiling): upload `best`
+  GH_CUDA(cudaMalloc(&pl.tiles_d, sizeof(TileDesc) * best.tiles.size()));
+  GH_CUDA(cudaMemcpyAsync(pl.tiles_d, best.tiles.data(), sizeof(TileDesc) * best.tiles.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  cudaFree(tiles_d);
+  GH_CUDA(cudaMalloc(&pl.win_d, sizeof(int4) * best.win.size()));
+  GH_CUDA(cudaMemcpyAsync(pl.win_d, best.win.data(), sizeof(int4) * best.win.size(),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  pl.n_tiles = static_cast<int>(best.tiles.size());
+  pl.max_rows = best.max_rows;
+  pl.n_entries = best.entries;
+  pl.vals_bytes = best.vals;
+  pl.pick_blocks = best.blocks;
+  GH_CUDA(cudaMalloc(&pl.rows_d, sizeof(uint16_t) * pl.n_entries * pl.p4));
+  GH_CUDA(cudaMemsetAsync(pl.rows_d, 0, sizeof(uint16_t) * pl.n_entries * pl.p4, ctx->stream));
+  int* err_d = nullptr;
+  GH_CUDA(cudaMalloc(&err_d, sizeof(int)));
+  GH_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), ctx->stream));
+  FillArgs f{};
+  f.tiles = pl.tiles_d;
+  f.grid = g;
+  f.win = pl.win_d;
+  f.idx = t->idx_d;
+  f.coef = t->coef_d;
+  f.P = P;
+  f.K = 1;
+  f.M = M;
+  f.p4 = pl.p4;
+  f.k3 = 0;
+  f.lanes = 2;
+  f.G = t->G;
+  f.bin0 = 0;
+  f.rows = pl.rows_d;
+  f.n_entries = pl.n_entries;
+  f.coef3 = nullptr;
+  f.err = err_d;
+  k_fill_plan<<<pl.n_tiles, 256, 0, ctx->stream>>>(f);
+  GH_LAUNCHED(ctx);
+  int herr = 0;
+  GH_CUDA(cudaMemcpyAsync(&herr, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(err_d);
+  if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
+  pl.built = true;
+  return &pl;
 }
 
 }  // namespace gh

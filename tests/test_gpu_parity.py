@@ -443,3 +443,31 @@ def test_c5_geometry_3d_and_grid_sharding(ctx):
         keys = np.maximum(keys, D.encode_keys(vx.cpu().numpy(), ix.cpu().numpy()))
     bins, _ = D.decode_keys(keys)
     assert np.array_equal(bins, g_idx.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["small", "c2"])
+def test_full_ring_exact_ties_smallest_bin(ctx, name):
+    # Full-ring plans (c1/c2-like, P <= 8) run bank-permuted entries, so
+    # entry order is not bin order. Exact ties must still resolve to the
+    # smallest bin (argmax_index, src/direct.cpp:55-62): all-zero frames tie
+    # every bin at 0 -> bin 0; a mirror-symmetric scene ties mirrored bins.
+    sc = S.small() if name == "small" else S.baseline("c2")
+    t = gh.precompute_hop_table(ctx, sc)
+    T = 40
+    zero = torch.zeros((T, sc.n_pairs, sc.n_samples), dtype=torch.complex64, device="cuda")
+    idx, val = gh.hop_argmax(ctx, t, zero)
+    assert (idx.cpu().numpy() == 0).all() and (val.cpu().numpy() == 0).all()
+    # mirror symmetry about the x axis: TX on the axis, RX pairs (x, +-y)
+    rx = np.array([[30.0, 0.0, 0.0], [-10.0, 25.0, 0.0], [-10.0, -25.0, 0.0]])
+    tx = np.zeros((3, 3))
+    sym = sc.with_(tx=tx, rx=rx, grid_n=(sc.grid_n[0], sc.grid_n[1], 1))
+    ts = gh.precompute_hop_table(ctx, sym)
+    fr, _ = O.synth(sym, 0, T)
+    fr = fr[:, [0, 2, 1], :]  # swap the mirrored receivers: map(x, y) -> map(x, -y)
+    fr = 0.5 * (fr + O.synth(sym, 0, T)[0])  # symmetrised frames
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, ts, fd).cpu().numpy()
+    idx = gh.hop_argmax(ctx, ts, fd)[0].cpu().numpy()
+    for k in range(T):
+        top = np.flatnonzero(m[k] == m[k].max())
+        assert idx[k] == top[0], (k, idx[k], top[:4])
