@@ -314,6 +314,38 @@ int gh_direct_argmax_d(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                        const float* frames_d, int32_t n_trials, int32_t combine,
                        int64_t* idx_d, float* val_d);
 
+/* ---- host-buffer stage entry points ---------------------------------------
+ * The reference signatures of the C++ wrappers (gridhop_b200.hpp) on HOST
+ * complex128 arrays (the reference's CMat element type); the computation is
+ * the device path of the _d forms (fp32 spectra and maps, fp64 table fits).
+ *   gh_spectra          fast_time_spectra (hopping.hpp:14): [T][P][N] -> [T][P][M]
+ *   gh_hop_map          hop_decision_map (hopping.hpp:22): -> map fp64 [T][G]
+ *   gh_direct_map       location_decision_map (direct.hpp:19-23)
+ *   gh_direct_estimate  direct_estimate location stage (direct.hpp:37-39)
+ *   gh_synth            synthesize_frame + add_noise (synth.hpp:26-36) of the
+ *                       campaign scene model; truth fp64 [T][K][3] (nullable)
+ *   gh_add_noise        add_noise (synth.hpp:29-36): the per-(trial, pair)
+ *                       substream draws, sigma = 10^(-snr/20); snr NaN: none
+ *   gh_fit_atom         fit_atom (interp.hpp:41) of n ranges: idx [n][3],
+ *                       coef complex128 [n][3], residual [n] (unused slots 0)
+ *   gh_table_geometry   the table's n_samples, os_range and B / c           */
+int gh_table_geometry(const gh_table* t, int32_t* n_samples, int32_t* os_range,
+                      double* range_scale);
+int gh_spectra(gh_ctx* ctx, const double* frames, int32_t n_trials, int32_t n_pairs,
+               int32_t n_samples, int32_t os_range, double* spectra);
+int gh_hop_map(gh_ctx* ctx, gh_table* t, const double* frames, int32_t n_trials, int32_t combine,
+               double* map);
+int gh_direct_map(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const double* frames,
+                  int32_t n_trials, int32_t combine, double* map);
+int gh_direct_estimate(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const double* frames,
+                       int32_t n_trials, int32_t combine, int64_t* idx, double* val);
+int gh_synth(gh_ctx* ctx, const gh_wave* wave, const gh_campaign* camp, uint64_t trial0,
+             int32_t n_trials, int32_t wrap, double* frames, double* truth);
+int gh_add_noise(gh_ctx* ctx, double* frames, int32_t n_trials, int32_t n_pairs, int32_t n_samples,
+                 uint64_t seed, uint64_t trial0, double snr_db);
+int gh_fit_atom(gh_ctx* ctx, int32_t n_samples, int32_t os_range, const double* r, int32_t n,
+                int32_t scheme, uint32_t* idx, double* coef, double* residual);
+
 /* ---- multi-GPU communicator ---------------------------------------------
  * One process per GPU. Rank 0 creates an id (ncclGetUniqueId), the caller
  * sends it to the other ranks (e.g. torch.distributed broadcast), and every
@@ -366,6 +398,13 @@ typedef struct {
   int32_t batch;              /* trials per device batch, 0: automatic       */
   const char* trial_csv;      /* nullable                                    */
   const char* summary_csv;    /* nullable                                    */
+  /* TableSource (montecarlo.hpp:43-45): when set, supplies the hop table of
+   * each density (e.g. a GHT1 file through gh_table_load) instead of the
+   * device build; the caller keeps ownership; *offline_ns is reported as the
+   * cell's table acquisition time. */
+  gh_table* (*table_source)(void* user, double density, const gh_grid* grid,
+                            int64_t* offline_ns);
+  void* table_source_user;
 } gh_campaign_desc;
 typedef struct {
   int32_t algorithm, density_idx, snr_idx, n_thresholds;

@@ -91,7 +91,8 @@ class CampaignDesc(C.Structure):
                 ("density", C.POINTER(C.c_double)), ("n_thresholds", C.c_int32),
                 ("thresholds_m", C.POINTER(C.c_double)), ("n_trials", C.c_int64),
                 ("topk", C.c_int32), ("batch", C.c_int32), ("trial_csv", C.c_char_p),
-                ("summary_csv", C.c_char_p)]
+                ("summary_csv", C.c_char_p), ("table_source", C.c_void_p),
+                ("table_source_user", C.c_void_p)]
 
 
 class CellStats(C.Structure):
@@ -776,7 +777,7 @@ def campaign_run(ctx: Context, scene: Scene, n_trials: int | None = None, algori
         arr = (C.c_double * len(thresholds))(*[float(x) for x in thresholds])
         keep.append(arr)
         d.n_thresholds, d.thresholds_m = len(thresholds), arr
-    d.n_trials = int(n_trials or scene.trials)
+    d.n_trials = int(scene.trials if n_trials is None else n_trials)
     d.topk = int(topk or scene.topk)
     d.batch = int(batch)
     d.trial_csv = str(trial_csv).encode() if trial_csv else None

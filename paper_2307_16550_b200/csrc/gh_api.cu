@@ -118,6 +118,7 @@ void free_table(gh::Table* t) {
     cudaFree(pl->coef3_d);
     cudaFree(pl->binid_d);
     cudaFree(pl->crow_d);
+    cudaFree(pl->pos_d);
   }
   delete t;
 }
@@ -311,6 +312,42 @@ __global__ void k_c128_to_c64(const double2* in, float2* out, int64_t n) {
   }
 }
 
+
+__global__ void k_c64_to_c128(const float2* in, double2* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 v = in[i];
+    out[i] = make_double2((double)v.x, (double)v.y);
+  }
+}
+
+__global__ void k_f32_to_f64(const float* in, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
+int grid_blocks(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 148LL * 16)); }
+
+// host complex128 -> device complex64 (scratch `b`, bytes for both forms)
+float2* frames_to_device(gh::Ctx* c, gh::Buffer& b, const double* frames, int64_t n) {
+  auto* base = static_cast<unsigned char*>(b.get(sizeof(double2) * n + sizeof(float2) * n));
+  auto* d128 = reinterpret_cast<double2*>(base);
+  auto* d64 = reinterpret_cast<float2*>(base + sizeof(double2) * n);
+  GH_CUDA(cudaMemcpyAsync(d128, frames, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+  k_c128_to_c64<<<grid_blocks(n), 256, 0, c->stream>>>(d128, d64, n);
+  GH_LAUNCHED(c);
+  return d64;
+}
+
+// device fp32 values -> host fp64
+void values_to_host(gh::Ctx* c, gh::Buffer& b, const float* v_d, int64_t n, double* out) {
+  auto* d = static_cast<double*>(b.get(sizeof(double) * n));
+  k_f32_to_f64<<<grid_blocks(n), 256, 0, c->stream>>>(v_d, d, n);
+  GH_LAUNCHED(c);
+  GH_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  GH_CUDA(cudaStreamSynchronize(c->stream));
+}
 
 // Host complex128 frames [T][P][N] (the reference's FrameSet element type)
 // -> host results [T][k], pipelined over trial chunks: the H2D copy of chunk
@@ -1389,6 +1426,193 @@ int gh_campaign_run(gh_ctx* ctx, gh_comm* comm, const gh_campaign_desc* desc, gh
     if (!c) fail(GH_EINVAL, "campaign: null argument");
     use_device(c);
     gh::campaign_run(c, reinterpret_cast<gh::Comm*>(comm), desc, out, capacity, n_cells);
+  });
+}
+
+}  // extern "C"
+
+// ---- host-buffer forms of the stage entry points (the C++ wrappers'
+// reference signatures: synth.hpp:26-36, hopping.hpp:14-22, direct.hpp:19-39,
+// interp.hpp:41). complex128 in / out as the reference's CMat; the compute
+// runs on the device in fp32 (fp64 for the table / fit) as the _d forms.
+extern "C" {
+
+int gh_table_geometry(const gh_table* table, int32_t* n_samples, int32_t* os_range,
+                      double* range_scale) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<const gh::Table*>(table);
+    if (!t) fail(GH_EINVAL, "hop table: null argument");
+    if (n_samples) *n_samples = t->N;
+    if (os_range) *os_range = t->os;
+    if (range_scale) *range_scale = t->scale;
+  });
+}
+
+int gh_spectra(gh_ctx* ctx, const double* frames, int32_t n_trials, int32_t n_pairs,
+               int32_t n_samples, int32_t os_range, double* spectra) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!frames || !spectra))) fail(GH_EINVAL, "spectra: null argument");
+    if (os_range < 1) fail(GH_EINVAL, "spectra: oversampling must be >= 1");
+    if (n_pairs < 1 || n_samples < 2 || n_trials < 0) fail(GH_EINVAL, "spectra: bad frame shape");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer in, out;
+    const int64_t rows = (int64_t)n_trials * n_pairs, M = (int64_t)n_samples * os_range;
+    const float2* f = frames_to_device(c, in, frames, rows * n_samples);
+    auto* base = static_cast<unsigned char*>(out.get((sizeof(float2) + sizeof(double2)) * rows * M));
+    auto* s64 = reinterpret_cast<float2*>(base);
+    auto* s128 = reinterpret_cast<double2*>(base + sizeof(float2) * rows * M);
+    gh::launch_fft(c, f, nullptr, n_trials, n_pairs, n_samples, os_range, 16, gh::FFT_NATURAL, s64);
+    k_c64_to_c128<<<grid_blocks(rows * M), 256, 0, c->stream>>>(s64, s128, rows * M);
+    GH_LAUNCHED(c);
+    GH_CUDA(cudaMemcpyAsync(spectra, s128, sizeof(double2) * rows * M, cudaMemcpyDeviceToHost,
+                            c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_hop_map(gh_ctx* ctx, gh_table* table, const double* frames, int32_t n_trials,
+               int32_t combine, double* map) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!c || !t || (n_trials > 0 && (!frames || !map))) fail(GH_EINVAL, "hop: null argument");
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer in, m32, m64;
+    const float2* f = frames_to_device(c, in, frames, (int64_t)n_trials * t->P * t->N);
+    auto* m = static_cast<float*>(m32.get(sizeof(float) * n_trials * t->G));
+    void* spec = gather_spectra(c, t, f, nullptr, n_trials, combine, true);
+    gh::launch_gather(c, t, spec, n_trials, combine, m, nullptr);
+    values_to_host(c, m64, m, (int64_t)n_trials * t->G, map);
+  });
+}
+
+int gh_direct_map(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const double* frames,
+                  int32_t n_trials, int32_t combine, double* map) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!frames || !map))) fail(GH_EINVAL, "decision: null argument");
+    check_wave(wave);
+    const int64_t G = grid_size(grid);
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer in, txrx, m32, m64;
+    const float2* f = frames_to_device(c, in, frames, (int64_t)n_trials * wave->n_pairs * wave->n_samples);
+    const double* tr = upload_txrx(c, wave, txrx);
+    auto* m = static_cast<float*>(m32.get(sizeof(float) * n_trials * G));
+    gh::direct_map(c, tr, wave, grid, f, n_trials, combine, m, nullptr);
+    values_to_host(c, m64, m, (int64_t)n_trials * G, map);
+  });
+}
+
+int gh_direct_estimate(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, const double* frames,
+                       int32_t n_trials, int32_t combine, int64_t* idx, double* val) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && (!frames || !idx || !val))) fail(GH_EINVAL, "decision: null argument");
+    check_wave(wave);
+    grid_size(grid);
+    check_combine(combine);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer in, txrx, res, v64;
+    const float2* f = frames_to_device(c, in, frames, (int64_t)n_trials * wave->n_pairs * wave->n_samples);
+    const double* tr = upload_txrx(c, wave, txrx);
+    auto* base = static_cast<unsigned char*>(
+        res.get((sizeof(unsigned long long) + sizeof(int64_t) + sizeof(float)) * n_trials));
+    auto* keys = reinterpret_cast<unsigned long long*>(base);
+    auto* di = reinterpret_cast<int64_t*>(keys + n_trials);
+    auto* dv = reinterpret_cast<float*>(di + n_trials);
+    GH_CUDA(cudaMemsetAsync(keys, 0, sizeof(unsigned long long) * n_trials, c->stream));
+    gh::direct_map(c, tr, wave, grid, f, n_trials, combine, nullptr, keys);
+    gh::launch_decode_keys(c, keys, n_trials, di, dv);
+    GH_CUDA(cudaMemcpyAsync(idx, di, sizeof(int64_t) * n_trials, cudaMemcpyDeviceToHost, c->stream));
+    values_to_host(c, v64, dv, n_trials, val);
+  });
+}
+
+int gh_synth(gh_ctx* ctx, const gh_wave* wave, const gh_campaign* camp, uint64_t trial0,
+             int32_t n_trials, int32_t wrap, double* frames, double* truth) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && !frames)) fail(GH_EINVAL, "synth: null argument");
+    check_wave(wave);
+    if (n_trials < 0) fail(GH_EINVAL, "trials must be >= 0");
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer txrx, buf;
+    const int64_t n = (int64_t)n_trials * wave->n_pairs * wave->n_samples;
+    const int64_t nt = (int64_t)n_trials * camp->n_targets * 3;
+    auto* base = static_cast<unsigned char*>(
+        buf.get(sizeof(float2) * n + sizeof(double2) * n + sizeof(double) * nt));
+    auto* f64 = reinterpret_cast<float2*>(base);
+    auto* f128 = reinterpret_cast<double2*>(base + sizeof(float2) * n);
+    auto* tr_d = reinterpret_cast<double*>(base + sizeof(float2) * n + sizeof(double2) * n);
+    const double* tr = upload_txrx(c, wave, txrx);
+    const gh::SynthParams sp = make_synth(c, tr, wave->range_scale, camp, trial0, wrap);
+    gh::launch_synth(c, sp, n_trials, wave->n_pairs, wave->n_samples, f64, tr_d);
+    check_synth_flag(c, sp);
+    k_c64_to_c128<<<grid_blocks(n), 256, 0, c->stream>>>(f64, f128, n);
+    GH_LAUNCHED(c);
+    GH_CUDA(cudaMemcpyAsync(frames, f128, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (truth)
+      GH_CUDA(cudaMemcpyAsync(truth, tr_d, sizeof(double) * nt, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_add_noise(gh_ctx* ctx, double* frames, int32_t n_trials, int32_t n_pairs, int32_t n_samples,
+                 uint64_t seed, uint64_t trial0, double snr_db) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n_trials > 0 && !frames)) fail(GH_EINVAL, "noise: null argument");
+    if (n_trials < 0 || n_pairs < 1 || n_samples < 1) fail(GH_EINVAL, "noise: bad frame shape");
+    if (!std::isfinite(snr_db)) return;  // NoiseSpec without SNR: noiseless (synth.cpp:41)
+    if (n_trials == 0) return;
+    use_device(c);
+    gh::Buffer buf;
+    const int64_t n = (int64_t)n_trials * n_pairs * n_samples;
+    auto* d = static_cast<double2*>(buf.get(sizeof(double2) * n));
+    GH_CUDA(cudaMemcpyAsync(d, frames, sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    gh::launch_add_noise(c, d, n_trials, n_pairs, n_samples, seed, trial0,
+                         std::pow(10.0, -snr_db / 20.0));
+    GH_CUDA(cudaMemcpyAsync(frames, d, sizeof(double2) * n, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int gh_fit_atom(gh_ctx* ctx, int32_t n_samples, int32_t os_range, const double* r, int32_t n,
+                int32_t scheme, uint32_t* idx, double* coef, double* residual) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c || (n > 0 && (!r || !idx || !coef || !residual))) fail(GH_EINVAL, "fit: null argument");
+    if (n_samples < 2) fail(GH_EINVAL, "waveform: n_samples must be >= 2");
+    if (os_range < 1) fail(GH_EINVAL, "hop table: oversampling must be >= 1");
+    if (scheme < GH_NEAREST || scheme > GH_POLAR) fail(GH_EINVAL, "unknown interpolation scheme");
+    for (int32_t i = 0; i < n; ++i)
+      if (!std::isfinite(r[i])) fail(GH_EINVAL, "fit_atom: range must be finite");
+    if (n <= 0) return;
+    use_device(c);
+    gh::Buffer buf;
+    auto* base = static_cast<unsigned char*>(
+        buf.get(sizeof(double) * n + sizeof(uint32_t) * 3 * n + sizeof(double2) * 3 * n + sizeof(double) * n));
+    auto* rd = reinterpret_cast<double*>(base);
+    auto* cd = reinterpret_cast<double2*>(base + sizeof(double) * n);
+    auto* res = reinterpret_cast<double*>(base + sizeof(double) * n + sizeof(double2) * 3 * n);
+    auto* id = reinterpret_cast<uint32_t*>(base + 2 * sizeof(double) * n + sizeof(double2) * 3 * n);
+    GH_CUDA(cudaMemcpyAsync(rd, r, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    gh::launch_fit_atoms(c, n_samples, os_range, rd, n, scheme, id, cd, res);
+    GH_CUDA(cudaMemcpyAsync(idx, id, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaMemcpyAsync(coef, cd, sizeof(double2) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaMemcpyAsync(residual, res, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

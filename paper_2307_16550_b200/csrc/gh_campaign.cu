@@ -321,6 +321,7 @@ void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* 
   auto* acc = static_cast<double*>(acc_b.get(sizeof(double) * (ns + 1)));
 
   Table* table = nullptr;
+  bool table_owned = true;
   try {
     int cell = 0;
     for (size_t di = 0; di < dens.size(); ++di) {
@@ -336,11 +337,19 @@ void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* 
       double offline_ms = 0.0;
       bool want_hop = false;
       for (int i = 0; i < n_algo; ++i) want_hop |= d->algorithms[i] == GH_ALGO_HOP;
-      if (table) {
-        op_free_table(table);
-        table = nullptr;
-      }
-      if (want_hop) {  // one table per density (montecarlo.cpp:116-136), built on the device
+      if (table && table_owned) op_free_table(table);
+      table = nullptr;
+      bool own_table = true;
+      if (want_hop && d->table_source) {  // the caller's TableSource (montecarlo.cpp:125-128)
+        int64_t ns_off = 0;
+        table = reinterpret_cast<Table*>(d->table_source(d->table_source_user, dens[di], &grid,
+                                                         &ns_off));
+        if (!table) fail(GH_ERUNTIME, "campaign: the table source returned no table");
+        if (table->P != P || table->G != G || table->N != N || table->M != M)
+          fail(GH_ERUNTIME, "stale hop table (grid size mismatch)");
+        own_table = false;
+        offline_ms = (double)ns_off * 1e-6;
+      } else if (want_hop) {  // one table per density (montecarlo.cpp:116-136), built on the device
         GH_CUDA(cudaEventRecord(e0, c->stream));
         table = op_new_table(c, &d->wave, &grid, d->scheme);
         table->wrap = d->wrap ? 1 : 0;
@@ -351,6 +360,7 @@ void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* 
         GH_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         offline_ms = ms;
       }
+      table_owned = own_table;
       for (size_t si = 0; si < snrs.size(); ++si) {
         gh_campaign camp = d->scene;
         if (snr_list) {
@@ -563,12 +573,12 @@ void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* 
       }
     }
   } catch (...) {
-    if (table) op_free_table(table);
+    if (table && table_owned) op_free_table(table);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     throw;
   }
-  if (table) op_free_table(table);
+  if (table && table_owned) op_free_table(table);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rank != 0) return;

@@ -154,6 +154,27 @@ __global__ void k_synth(SynthParams sp, int T, int P, int N, float2* frames,
   }
 }
 
+// add_noise (synth.cpp:39-49) on caller frames, complex128 [T][P][N]: the
+// synthesis' noise draws (substream (seed, trial, p), draws 2n and 2n + 1;
+// rng.hpp complex_gaussian) in fp64, sigma = 10^(-snr / 20) (alpha_ref 1)
+__global__ void k_add_noise(double2* frames, int T, int P, int N, uint64_t seed, uint64_t trial0,
+                            double sigma) {
+  const int64_t total = (int64_t)T * P * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(e % N);
+    const int p = (int)((e / N) % P);
+    const int64_t t = e / ((int64_t)N * P);
+    const uint64_t key = substream(seed, trial0 + (uint64_t)t, (uint64_t)p);
+    const double u1 = uniform01(key, 2ull * n), u2 = uniform01(key, 2ull * n + 1);
+    const double amp = sigma * sqrt(-log1p(-u1));
+    double s, c;
+    sincospi(2.0 * u2, &s, &c);
+    frames[e].x += amp * c;
+    frames[e].y += amp * s;
+  }
+}
+
 // ------------------------------------------------------------ FFT core
 
 // cos / sin of 2 pi e / 16
@@ -1142,6 +1163,14 @@ void launch_synth(Ctx* ctx, const SynthParams& sp, int T, int P, int N, float2* 
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
   KTimer kt(ctx, "synth");
   k_synth<<<blocks, 256, 0, ctx->stream>>>(sp, T, P, N, frames_d, truth_d);
+  GH_LAUNCHED(ctx);
+}
+
+void launch_add_noise(Ctx* ctx, double2* frames_d, int T, int P, int N, uint64_t seed,
+                      uint64_t trial0, double sigma) {
+  const int64_t total = (int64_t)T * P * N;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148LL * 16));
+  k_add_noise<<<blocks, 256, 0, ctx->stream>>>(frames_d, T, P, N, seed, trial0, sigma);
   GH_LAUNCHED(ctx);
 }
 

@@ -646,6 +646,7 @@ struct TopkArgs {
   unsigned vals_off;         // byte offsets in dynamic shared memory
   unsigned lists_off;        // per-warp lists, first the block maxima [TB][bmax]
   int bmax;                  // block-maximum slots per trial
+  const uint16_t* pos;       // [entries] values-buffer position (plan pos_d)
 };
 
 __device__ __forceinline__ uint32_t ord_f(float v) {
@@ -754,9 +755,7 @@ __global__ void __launch_bounds__(kTopkNW * 32, 1) k_gather_topk(GatherArgs a, T
             }
           }
           if (!check || j < nblk) {
-            int64_t lx, ly, lz;
-            tile_local(td, lb, &lx, &ly, &lz);
-            const int pos = ((int)lz * td.wy + (int)ly) * pitch + (int)lx;
+            const int pos = __ldg(tk.pos + entry0 + lb);
             reinterpret_cast<float4*>(vals)[pos * 2 + v] =
                 make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
           }
@@ -878,22 +877,38 @@ __global__ void __launch_bounds__(kTopkNW * 32, 1) k_gather_topk(GatherArgs a, T
     // keys >= the prune key (the K-th key of K verified maxima)
     {
       unsigned long long thr = cta_thr[t];
-      const int ncore = td.cwx * td.cwy * td.cwz;
-      const int cxy = td.cwx * td.cwy;
-      for (int c0 = warp * 16; c0 < ncore; c0 += NW * 16) {
+      // chunks of 4 core x-positions: chunk q = (row q / nxc, x-segment
+      // q % nxc); warp w takes chunks w, w + NW, ... 4 at a time, tracked
+      // incrementally (no divisions in the loop)
+      const int nxc = (td.cwx + 3) >> 2, nq = nxc * td.cwy;
+      int qy = warp / nxc, qx = warp % nxc;  // chunk of u = 0
+      const int step_y = (4 * NW) / nxc, step_x = (4 * NW) % nxc;
+      for (int q0 = warp; q0 < nq; q0 += 4 * NW) {
         thr = max(thr, *reinterpret_cast<volatile unsigned long long*>(&cta_thr[t]));
         const float tv = thr ? __uint_as_float((uint32_t)(thr >> 32) & 0x7fffffffu) : -1.0f;
         float val[4];
         int px[4], py[4], pz[4];
+        int uy = qy, ux = qx;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int c = c0 + 4 * u + (lane >> 3);
-          const int cc = c < ncore ? c : ncore - 1;
-          pz[u] = cc / cxy + td.cz0;
-          py[u] = (cc % cxy) / td.cwx + td.cy0;
-          px[u] = cc % td.cwx + td.cx0;
-          val[u] = vals[((pz[u] * td.wy + py[u]) * pitch + px[u]) * TB + t];
-          if (c >= ncore) val[u] = -1.0f;
+          const int cx = 4 * ux + (lane >> 3);
+          const bool in = q0 + u * NW < nq && cx < td.cwx;
+          pz[u] = td.cz0;
+          py[u] = td.cy0 + (in ? uy : 0);
+          px[u] = td.cx0 + (in ? cx : 0);
+          val[u] = in ? vals[(py[u] * pitch + px[u]) * TB + t] : -1.0f;
+          ux += NW % nxc;
+          uy += NW / nxc;
+          if (ux >= nxc) {
+            ux -= nxc;
+            ++uy;
+          }
+        }
+        qx += step_x;
+        qy += step_y;
+        while (qx >= nxc) {
+          qx -= nxc;
+          ++qy;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1176,6 +1191,7 @@ void launch_gather_topk(Ctx* ctx, Table* t, const void* spec_d, int T, int K,
   tk.vals_off = static_cast<unsigned>(win_bytes);
   tk.lists_off = static_cast<unsigned>(win_bytes + (pl.vals_bytes + 127) / 128 * 128);
   tk.bmax = pl.pick_blocks;
+  tk.pos = pl.pos_d;
   const size_t pick = std::max<size_t>((size_t)kTopkNW * 8 * kTopkMaxK * 8,
                                        (size_t)pl.tb * pl.pick_blocks * 8);
   const size_t smem = tk.lists_off + pick;

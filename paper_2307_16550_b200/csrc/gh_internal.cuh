@@ -188,6 +188,7 @@ struct Plan {
   bool halo = false;
   size_t vals_bytes = 0;   // the largest tile's [pitch * wy * wz][tb] fp32 values
   int pick_blocks = 0;     // the largest tile's 4 x 4 core blocks (prune seeds)
+  uint16_t* pos_d = nullptr;  // [entries] values-buffer position of each entry
 };
 
 struct Table {
@@ -308,6 +309,10 @@ void comm_destroy(Comm* cm);
 void comm_info(const Comm* cm, int* n_ranks, int* rank);
 void campaign_run(Ctx* c, Comm* comm, const gh_campaign_desc* d, gh_cell_stats* out,
                   int32_t capacity, int32_t* n_cells);
+void launch_fit_atoms(Ctx* ctx, int n_samples, int os, const double* r_d, int n, int scheme,
+                      uint32_t* idx_d, double2* coef_d, double* res_d);
+void launch_add_noise(Ctx* ctx, double2* frames_d, int T, int P, int N, uint64_t seed,
+                      uint64_t trial0, double sigma);
 // host operations of gh_api.cu used by the campaign driver (gh_campaign.cu)
 void op_check_wave(const gh_wave* w);
 int64_t op_grid_size(const gh_grid* g);

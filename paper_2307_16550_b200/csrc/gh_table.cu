@@ -242,6 +242,34 @@ __global__ void k_build(BuildArgs a) {
     atomicMax(a.max_res_bits, (unsigned long long)__double_as_longlong(worst));
 }
 
+// fit_atom for caller-chosen ranges (the reference's public fit_atom,
+// interp.hpp:41): one thread per range, the table builder's device code
+__global__ void k_fit_atoms(int n_samples, int os, const double* r, int n, int scheme,
+                           uint32_t* idx, double2* coef, double* res) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t ix[3] = {0u, 0u, 0u};
+  cd c[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  res[i] = fit_atom(n_samples, os, r[i], scheme, ix, c);
+  for (int j = 0; j < 3; ++j) {
+    idx[3 * i + j] = ix[j];
+    coef[3 * i + j] = make_double2(c[j].re, c[j].im);
+  }
+}
+
+// top-K plans: each entry's position in its tile's values buffer
+// ((lz * wy + ly) * pitch + lx), so the gather stores without decoding the
+// blocked entry order
+__global__ void k_fill_pos(const TileDesc* tiles, uint16_t* pos) {
+  const TileDesc td = tiles[blockIdx.x];
+  const int nb = td.wx * td.wy * td.wz, pitch = topk_pitch(td.wx);
+  for (int lb = threadIdx.x; lb < nb; lb += blockDim.x) {
+    int64_t lx, ly, lz;
+    tile_local(td, lb, &lx, &ly, &lz);
+    pos[td.entry_off + lb] = static_cast<uint16_t>((lz * td.wy + ly) * pitch + lx);
+  }
+}
+
 // smallest flagged entry index strictly above `after` (offender report)
 __global__ void k_next_flag(const uint8_t* flags, int64_t total, int64_t after,
                             unsigned long long* out) {
@@ -975,6 +1003,10 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
   f.err = err_d;
   k_fill_plan<<<pl.n_tiles, 256, 0, ctx->stream>>>(f);
   GH_LAUNCHED(ctx);
+  if (best.vals / (8 * sizeof(float)) > 65535) fail(GH_EINVAL, "gather plan: top-K tile too large");
+  GH_CUDA(cudaMalloc(&pl.pos_d, sizeof(uint16_t) * pl.n_entries));
+  k_fill_pos<<<pl.n_tiles, 256, 0, ctx->stream>>>(pl.tiles_d, pl.pos_d);
+  GH_LAUNCHED(ctx);
   int herr = 0;
   GH_CUDA(cudaMemcpyAsync(&herr, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -982,6 +1014,13 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
   if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
   pl.built = true;
   return &pl;
+}
+
+void launch_fit_atoms(Ctx* ctx, int n_samples, int os, const double* r_d, int n, int scheme,
+                      uint32_t* idx_d, double2* coef_d, double* res_d) {
+  k_fit_atoms<<<(n + 127) / 128, 128, 0, ctx->stream>>>(n_samples, os, r_d, n, scheme, idx_d,
+                                                        coef_d, res_d);
+  GH_LAUNCHED(ctx);
 }
 
 }  // namespace gh
