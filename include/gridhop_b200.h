@@ -108,6 +108,11 @@ int gh_ctx_reset_timing(gh_ctx* ctx);
  * checked and timed against); 2 = single-stage tcgen05 3xTF32 kernel (v1);
  * 3 = the warp-specialised pipeline in 3xTF32 (kind::tf32). */
 int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
+/* Top-K local-maximum engine (BASELINE c3): 0 = auto (the measured faster
+ * one: map then pick), 1 = fused gather + pick (maps stay in shared memory), 2 =
+ * map-mode gather then k_topk_localmax over the maps in HBM. Both return
+ * identical bins and values. */
+int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl);
 /* Diagnostics: measured shared-memory (LSU) read bandwidth of the device,
  * GB/s, all SMs — the roofline denominator of the gather kernel. */
 int gh_measure_smem_peak(gh_ctx* ctx, double* gbps);

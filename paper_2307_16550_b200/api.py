@@ -15,6 +15,7 @@ Error behaviour mirrors the reference's exception types:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
@@ -119,9 +120,10 @@ def exported_symbols() -> list[str]:
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
-            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build()")
-        L = C.CDLL(str(LIB_PATH))
+        path = Path(os.environ.get("GH_LIB_PATH", LIB_PATH))  # diagnostic builds (tools/)
+        if not path.exists():
+            raise ImportError(f"{path} is missing: run __graft_entry__.build()")
+        L = C.CDLL(str(path))
         vp, i32, i64, u64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
         P = C.POINTER
         sig = {
@@ -138,6 +140,7 @@ def lib() -> C.CDLL:
             "gh_ctx_reset_timing": (C.c_int, [vp]),
             "gh_measure_smem_peak": (C.c_int, [vp, P(f64)]),
             "gh_ctx_set_direct_impl": (C.c_int, [vp, i32]),
+            "gh_ctx_set_topk_impl": (C.c_int, [vp, i32]),
             "gh_table_build": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, P(vp)]),
             "gh_table_upload": (C.c_int, [vp, P(CWave), P(CGrid), i32, vp, vp, P(vp)]),
             "gh_table_build_shard": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, i32, i32, P(vp)]),
@@ -255,6 +258,11 @@ class Context:
 
     def reset_timing(self) -> None:
         _check(lib().gh_ctx_reset_timing(self.h))
+
+    def set_topk_impl(self, impl: str) -> None:
+        """'auto' (default), 'fused' (gather + local-maximum pick in shared
+        memory) or 'map' (map-mode gather, then k_topk_localmax on the maps)."""
+        _check(lib().gh_ctx_set_topk_impl(self.h, {"auto": 0, "fused": 1, "map": 2}[impl]))
 
     def set_direct_impl(self, impl: str) -> None:
         """'tcgen05' (default: warp-specialised 3xFP16 tensor-core pipeline),

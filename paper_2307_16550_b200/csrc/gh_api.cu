@@ -208,7 +208,10 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
 // gather launches fill the GPU), then k_topk_localmax picks the peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
-  if (gh::Plan* tp = gh::build_plan_topk(c, t)) {
+  // auto (0) takes the map-then-pick path until the fused kernel measures
+  // faster on c3 (top-K)
+  gh::Plan* tp = c->topk_impl != 1 ? nullptr : gh::build_plan_topk(c, t);
+  if (tp) {
     // fused: the gather keeps each tile's values in shared memory and picks
     // the tile's local maxima there; per (trial, tile) K keys, then a merge.
     // Trial chunks bound the spectra (~4 GB) and candidate (~1 GB) scratch.
@@ -698,6 +701,16 @@ int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl) {
            "ctx: direct impl must be 0 (tcgen05 3xFP16), 1 (simt), 2 (tcgen05 v1) or 3 (tcgen05 "
            "3xTF32)");
     c->direct_impl = impl;
+  });
+}
+
+int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    if (impl < 0 || impl > 2)
+      fail(GH_EINVAL, "ctx: top-k impl must be 0 (auto), 1 (fused) or 2 (map then pick)");
+    c->topk_impl = impl;
   });
 }
 

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 
+#include "gh_gather_common.cuh"
 #include "gh_internal.cuh"
 #include "gh_ptx.cuh"
 
@@ -41,29 +42,6 @@ using namespace ptx;
 // staging bytes per bin grow faster than the overlap gains.
 template <bool K3, bool FULL>
 constexpr int gather_threads() { return K3 ? 512 : 768; }
-
-struct GatherArgs {
-  const void* spec;       // [batches][P][M][TB] float or float2
-  const TileDesc* tiles;  // tiled plan
-  const int4* win;        // [tiles][P] / [P]
-  const uint16_t* rows;   // [p4 / 4][entries][4], 16-byte units (word-major)
-  int64_t n_entries;      // entries of the plan (word stride of rows)
-  const float2* coef3;    // [P][3][entries] (word-major)
-  const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
-  const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
-  int cbits;              // bits per ring row in crow
-  int ring;               // staged rows per pair (full-ring plan)
-  gh_grid grid;
-  int64_t G;              // bins of the table (shard)
-  int64_t bin0;           // global index of the shard's first bin
-  int n_batches;          // trial batches (full plan: persistent work split)
-  int n_tiles;            // tiled plan
-  int chunk_pairs;        // tiled plan: pairs per staging chunk
-  int full;
-  int P, p4, M, T;
-  float* map;             // parity mode [T][G]
-  unsigned long long* keys;
-};
 
 // PLAIN: the plan is known to run x-fastest (map-mode plans), so the
 // per-bin map stores skip the blocked-order decode
@@ -80,48 +58,6 @@ __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDes
     tile_local(td, lb, &lx, &ly, &lz);
   }
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
-}
-
-__device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y); }
-
-// value contribution of one pair for the lane's trials
-template <int TB, bool K3, bool MAG, int L>
-__device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsigned off16,
-                                           const float2* __restrict__ cf, float2 (&acc)[2],
-                                           bool first, int64_t cs = 0) {
-  if constexpr (!K3) {
-    const float4 z = smv[off16];
-    if (first) {
-      acc[0] = f2(z.x, z.y);
-      acc[1] = f2(z.z, z.w);
-    } else {
-      acc[0] = __fadd2_rn(acc[0], f2(z.x, z.y));
-      acc[1] = __fadd2_rn(acc[1], f2(z.z, z.w));
-    }
-  } else {
-    const float2 c0 = __ldg(cf), c1 = __ldg(cf + cs), c2 = __ldg(cf + 2 * cs);
-    const float4 z0 = smv[off16];
-    const float4 z1 = smv[off16 + L];
-    const float4 z2 = smv[off16 + 2 * L];
-    // trial a = (x, y), trial b = (z, w); v = sum_j c_j z_j (complex product)
-    float2 ra = __fmul2_rn(f2(c0.x, c0.x), f2(z0.x, z0.y));           // (c0r*zr, c0r*zi)
-    ra = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.y, z0.x), ra);              // (-c0i*zi, c0i*zr)
-    ra = __ffma2_rn(f2(c1.x, c1.x), f2(z1.x, z1.y), ra);
-    ra = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.y, z1.x), ra);
-    ra = __ffma2_rn(f2(c2.x, c2.x), f2(z2.x, z2.y), ra);
-    ra = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.y, z2.x), ra);
-    float2 rb = __fmul2_rn(f2(c0.x, c0.x), f2(z0.z, z0.w));
-    rb = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.w, z0.z), rb);
-    rb = __ffma2_rn(f2(c1.x, c1.x), f2(z1.z, z1.w), rb);
-    rb = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.w, z1.z), rb);
-    rb = __ffma2_rn(f2(c2.x, c2.x), f2(z2.z, z2.w), rb);
-    rb = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.w, z2.z), rb);
-    const float2 sq = __ffma2_rn(f2(ra.x, rb.x), f2(ra.x, rb.x),
-                                 __fmul2_rn(f2(ra.y, rb.y), f2(ra.y, rb.y)));
-    const float2 v = MAG ? f2(sqrtf(sq.x), sqrtf(sq.y)) : sq;
-    if (first) acc[0] = v;
-    else acc[0] = __fadd2_rn(acc[0], v);
-  }
 }
 
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
@@ -615,402 +551,6 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
   }
 }
 
-// ---- fused top-K (BASELINE c3): gather + local-maximum pick per tile.
-//
-// Halo plans (build_plan_topk): a tile's box is its core grown by one bin,
-// so the gather computes every value a core bin's local-maximum test reads.
-// Persistent CTAs walk (tile, batch) items batch-major. Per item:
-//  1. gather as k_gather (8-trial power rows, LDS.128 per pair, FADD2), but
-//     each bin's 8 values go to a shared-memory values buffer [pos][8]
-//     (pos = box coordinates, row pitch == 2 mod 4) instead of an argmax;
-//  2. barrier: the windows are dead, so thread 0 issues the next item's
-//     window staging (TMA bulk copies) — it lands under step 3;
-//  3. the pick: lane = (position, trial) reads 4 positions x 8 trials per
-//     128-byte wavefront; a value whose key (value bits << 32 | ~bin) beats
-//     the lane's prune key is tested against its 8 neighbours in shared
-//     memory (the rule of k_topk_localmax: > smaller-index neighbours, >=
-//     larger ones); local maxima enter per-(warp, trial) sorted lists. The
-//     prune key is the best K-th key of any full list (a CTA-shared atomic
-//     max per trial) or of a finished tile of the same trial (global), so
-//     pruning is exact;
-//  4. warp t merges the warps' lists of trial t into the tile's top-K keys
-//     cand[trial][tile][K]; launch_topk_merge reduces over tiles.
-// Maps never reach HBM (c3: 4 MB per trial otherwise).
-constexpr int kTopkNW = 24;  // warps (768 threads, one CTA per SM)
-constexpr int kTopkMaxK = 8;
-
-struct TopkArgs {
-  int K;
-  unsigned long long* cand;  // [T][n_tiles][K] keys, 0 = none
-  unsigned long long* thr;   // [T] prune keys (K-th key of a finished tile)
-  unsigned vals_off;         // byte offsets in dynamic shared memory
-  unsigned lists_off;        // per-warp lists, first the block maxima [TB][bmax]
-  int bmax;                  // block-maximum slots per trial
-  const uint16_t* pos;       // [entries] values-buffer position (plan pos_d)
-};
-
-__device__ __forceinline__ uint32_t ord_f(float v) {
-  const uint32_t b = __float_as_uint(v);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-
-template <int PC, int PQ>
-__global__ void __launch_bounds__(kTopkNW * 32, 1) k_gather_topk(GatherArgs a, TopkArgs tk) {
-  constexpr int TB = 8, L = 2, TPL = 4, BPW = 16, NW = kTopkNW;
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t stage_bar;
-  __shared__ unsigned long long cta_thr[TB];
-  __shared__ int bcnt[TB];
-  float* vals = reinterpret_cast<float*>(smraw + tk.vals_off);
-  unsigned long long* lists = reinterpret_cast<unsigned long long*>(smraw + tk.lists_off);
-  const int P = PC ? PC : a.P;
-  const int K = tk.K;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t n_items = (int64_t)a.n_tiles * a.n_batches;
-  if ((int64_t)blockIdx.x >= n_items) return;
-  const int nx = a.grid.n[0], ny = a.grid.n[1];
-
-  auto stage = [&](int64_t item) {  // thread 0: the item's windows by TMA
-    const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
-    const int4* win = a.win + (int64_t)tile * a.P;
-    const uint4* spec = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(a.spec) +
-                                                       (int64_t)tb * a.P * a.M * TB * 4);
-    uint4* sm4 = reinterpret_cast<uint4*>(smraw);
-    uint32_t total = 0;
-    for (int p = 0; p < P; ++p) total += (uint32_t)__ldg(&win[p].y) * 16u * L;
-    mbar_expect_tx(&stage_bar, total);
-    for (int p = 0; p < P; ++p) {
-      const int4 w = __ldg(&win[p]);
-      const uint4* src = spec + (int64_t)p * a.M * L;
-      uint4* dst = sm4 + (int64_t)w.z * L;
-      for (int r = 0, gi = w.x; r < w.y; gi = 0) {
-        const int n = a.M - gi < w.y - r ? a.M - gi : w.y - r;
-        bulk_g2s(dst + (int64_t)r * L, src + (int64_t)gi * L, (uint32_t)n * 16u * L, &stage_bar);
-        r += n;
-      }
-    }
-    mbar_arrive(&stage_bar);
-  };
-
-  if (threadIdx.x == 0) {
-    mbar_init(&stage_bar, 1);
-    mbar_fence_init();
-    stage(blockIdx.x);
-  }
-  if (threadIdx.x < TB) bcnt[threadIdx.x] = 0;
-  uint32_t phase = 0;
-  const int sub = lane / L, v = lane % L;
-  const float4* smv = reinterpret_cast<const float4*>(smraw) + v;
-  const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);
-  const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
-
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
-    const TileDesc td = a.tiles[tile];
-    const int64_t entry0 = td.entry_off;
-    const int nb = td.wx * td.wy * td.wz;
-    const int pitch = topk_pitch(td.wx);
-    if (threadIdx.x < TB) {
-      const int trial = tb * TB + threadIdx.x;
-      cta_thr[threadIdx.x] = trial < a.T ? tk.thr[trial] : ~0ull;
-    }
-    // ---- 1. gather the halo box into the values buffer
-    {
-      const int per_warp = ((nb + NW - 1) / NW + BPW - 1) / BPW * BPW;
-      const int w0 = warp * per_warp < nb ? warp * per_warp : nb;
-      const int w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
-      uint2 cur[PQ], nxt[PQ];
-#pragma unroll
-      for (int q = 0; q < PQ; ++q) cur[q] = nxt[q] = make_uint2(0u, 0u);
-      if (w0 + lane < w1) {
-#pragma unroll
-        for (int q = 0; q < PQ; ++q)
-          if (q < pq) cur[q] = __ldg(rows2 + q * a.n_entries + entry0 + w0 + lane);
-      }
-      mbar_wait(&stage_bar, phase);
-      phase ^= 1u;
-      for (int blk = w0; blk < w1; blk += 32) {
-        if (blk + 32 + lane < w1) {
-#pragma unroll
-          for (int q = 0; q < PQ; ++q)
-            if (q < pq) nxt[q] = __ldg(rows2 + q * a.n_entries + entry0 + blk + 32 + lane);
-        }
-        const int nblk = w1 - blk < 32 ? w1 - blk : 32;
-        auto step = [&](int s, bool check) {
-          const int j = s * BPW + sub;
-          const int lb = blk + (!check || j < nblk ? j : 0);
-          float2 acc[2];
-          acc[0] = acc[1] = f2(0.f, 0.f);
-#pragma unroll
-          for (int q = 0; q < PQ; ++q) {
-            if (q >= pq) break;
-            const unsigned ex = __shfl_sync(0xffffffffu, cur[q].x, j & 31);
-            const unsigned ey = __shfl_sync(0xffffffffu, cur[q].y, j & 31);
-            const unsigned o[4] = {ex & 0xffffu, ex >> 16, ey & 0xffffu, ey >> 16};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int p = 4 * q + u;
-              if (PC ? p >= PC : p >= a.P) break;
-              accumulate<TB, false, false, L>(smv, o[u], nullptr, acc, p == 0);
-            }
-          }
-          if (!check || j < nblk) {
-            const int pos = __ldg(tk.pos + entry0 + lb);
-            reinterpret_cast<float4*>(vals)[pos * 2 + v] =
-                make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
-          }
-        };
-        if (nblk == 32) {
-#pragma unroll
-          for (int s = 0; s < 32 / BPW; ++s) step(s, false);
-        } else {
-          for (int s = 0; s * BPW < nblk; ++s) step(s, true);
-        }
-#pragma unroll
-        for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
-      }
-    }
-    __syncthreads();  // values complete, windows no longer read
-    if (threadIdx.x == 0 && item + gridDim.x < n_items) stage(item + gridDim.x);
-
-    const int t = lane & 7;  // the pick's lane = (position, trial t)
-    const int trial = tb * TB + t;
-    const int nzz = a.grid.n[2];
-    // local-maximum test of box position (px, py, pz), trial t, value cv,
-    // on its neighbours in the values buffer (the rule of k_topk_localmax)
-    auto is_lm = [&](int px, int py, int pz, float cv) {
-      const int gx = td.x0 + px, gy = td.y0 + py, gz = td.z0 + pz;
-      for (int dz = -1; dz <= 1; ++dz) {
-        if (gz + dz < 0 || gz + dz >= nzz) continue;
-        for (int dy = -1; dy <= 1; ++dy) {
-          if (gy + dy < 0 || gy + dy >= ny) continue;
-          for (int dx = -1; dx <= 1; ++dx) {
-            if ((dx | dy | dz) == 0 || gx + dx < 0 || gx + dx >= nx) continue;
-            const float nv = vals[(((pz + dz) * td.wy + (py + dy)) * pitch + (px + dx)) * TB + t];
-            const bool smaller = dz < 0 || (dz == 0 && (dy < 0 || (dy == 0 && dx < 0)));
-            if (smaller ? !(cv > nv) : !(cv >= nv)) return false;
-          }
-        }
-      }
-      return true;
-    };
-    auto mkey = [&](float v, int px, int py, int pz) {
-      const int64_t gb = (int64_t)(td.x0 + px) +
-                         (int64_t)nx * ((td.y0 + py) + (int64_t)ny * (td.z0 + pz));
-      return ((unsigned long long)ord_f(v) << 32) | (0xffffffffull - (uint64_t)gb);
-    };
-    // ---- 3a. prune seed: the key maximum of each 4 x 4 block of the core
-    // is a local maximum of the map when all its neighbours lie inside the
-    // block (or are smaller); distinct blocks give distinct maxima, so the
-    // K-th best verified block maximum bounds the tile's K-th local maximum
-    // from below, before any per-bin test (2-D tiles: cwz = 1)
-    {
-      unsigned long long* bkeys = lists;  // [TB][bmax] (shares the list region)
-      const int nbx = (td.cwx + 3) >> 2, nby = (td.cwy + 3) >> 2;
-      const int j = lane >> 3;
-      for (int blk = warp; blk < nbx * nby; blk += NW) {
-        const int bx = blk % nbx, by = blk / nbx;
-        const int cx = bx * 4 + j;
-        unsigned long long best = 0ull;
-        int bpx = 0, bpy = 0;
-        float bv = 0.f;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int cy = by * 4 + r;
-          if (cx < td.cwx && cy < td.cwy) {
-            const int px = td.cx0 + cx, py = td.cy0 + cy;
-            const float v = vals[(py * pitch + px) * TB + t];
-            const unsigned long long k = mkey(v, px, py, td.cz0);
-            if (k > best) {
-              best = k;
-              bpx = px;
-              bpy = py;
-              bv = v;
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 8; o < 32; o <<= 1) {
-          const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int ox = __shfl_xor_sync(0xffffffffu, bpx, o);
-          const int oy = __shfl_xor_sync(0xffffffffu, bpy, o);
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          if (ob > best) {
-            best = ob;
-            bpx = ox;
-            bpy = oy;
-            bv = ov;
-          }
-        }
-        if (j == 0 && best && trial < a.T && is_lm(bpx, bpy, td.cz0, bv))
-          bkeys[t * tk.bmax + atomicAdd(&bcnt[t], 1)] = best;
-      }
-    }
-    __syncthreads();
-    if (warp < TB) {  // 3b. warp t: the K-th best verified block maximum of trial t
-      const unsigned long long* bk = lists + warp * tk.bmax;
-      const int n = bcnt[warp];
-      unsigned long long prev = ~0ull;
-      for (int k = 0; k < K && n >= K; ++k) {
-        unsigned long long m = 0ull;
-        for (int i = lane; i < n; i += 32) {
-          const unsigned long long x = bk[i];
-          if (x < prev && x > m) m = x;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long om = __shfl_xor_sync(0xffffffffu, m, o);
-          m = om > m ? om : m;
-        }
-        prev = m;
-      }
-      if (lane == 0) {
-        if (n >= K && prev > cta_thr[warp]) cta_thr[warp] = prev;
-        bcnt[warp] = 0;
-      }
-    }
-    __syncthreads();
-    // warp lists of this item: [warp][trial][kTopkMaxK], 0 = empty
-    for (int i = lane; i < TB * kTopkMaxK; i += 32) lists[warp * TB * kTopkMaxK + i] = 0ull;
-    __syncwarp();
-
-    // ---- 3c. pick: lane = (position c + lane / 8, trial t); candidates are
-    // keys >= the prune key (the K-th key of K verified maxima)
-    {
-      unsigned long long thr = cta_thr[t];
-      // chunks of 4 core x-positions: chunk q = (row q / nxc, x-segment
-      // q % nxc); warp w takes chunks w, w + NW, ... 4 at a time, tracked
-      // incrementally (no divisions in the loop)
-      const int nxc = (td.cwx + 3) >> 2, nq = nxc * td.cwy;
-      int qy = warp / nxc, qx = warp % nxc;  // chunk of u = 0
-      const int step_y = (4 * NW) / nxc, step_x = (4 * NW) % nxc;
-      for (int q0 = warp; q0 < nq; q0 += 4 * NW) {
-        thr = max(thr, *reinterpret_cast<volatile unsigned long long*>(&cta_thr[t]));
-        const float tv = thr ? __uint_as_float((uint32_t)(thr >> 32) & 0x7fffffffu) : -1.0f;
-        float val[4];
-        int px[4], py[4], pz[4];
-        int uy = qy, ux = qx;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cx = 4 * ux + (lane >> 3);
-          const bool in = q0 + u * NW < nq && cx < td.cwx;
-          pz[u] = td.cz0;
-          py[u] = td.cy0 + (in ? uy : 0);
-          px[u] = td.cx0 + (in ? cx : 0);
-          val[u] = in ? vals[(py[u] * pitch + px[u]) * TB + t] : -1.0f;
-          ux += NW % nxc;
-          uy += NW / nxc;
-          if (ux >= nxc) {
-            ux -= nxc;
-            ++uy;
-          }
-        }
-        qx += step_x;
-        qy += step_y;
-        while (qx >= nxc) {
-          qx -= nxc;
-          ++qy;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          bool cand = val[u] >= tv && trial < a.T;
-          unsigned long long key = 0ull;
-          if (cand) {
-            key = mkey(val[u], px[u], py[u], pz[u]);
-            cand = key >= thr && is_lm(px[u], py[u], pz[u], val[u]);
-          }
-          unsigned ver = __ballot_sync(0xffffffffu, cand);
-          while (ver) {  // insert the verified maxima into their warp lists
-            const int src = __ffs(ver) - 1;
-            ver &= ver - 1;
-            const unsigned long long ck = __shfl_sync(0xffffffffu, key, src);
-            const int ct = src & 7;
-            unsigned long long* cl = lists + ((int64_t)warp * TB + ct) * kTopkMaxK;
-            const unsigned long long e = lane < K ? cl[lane] : 0ull;
-            const int pos = __popc(__ballot_sync(0xffffffffu, lane < K && e > ck));
-            const unsigned long long up = __shfl_up_sync(0xffffffffu, e, 1);
-            __syncwarp();
-            if (lane < K && pos < K) {
-              if (lane > pos) cl[lane] = up;
-              if (lane == pos) cl[lane] = ck;
-            }
-            __syncwarp();
-            const unsigned long long kth = cl[K - 1];
-            if (kth) {
-              if (lane == 0) atomicMax(&cta_thr[ct], kth);
-              if (t == ct) thr = max(thr, kth);
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    // ---- 4. tile top-K per trial: warp t merges the NW warp lists
-    if (warp < TB) {
-      const int t = warp, trial = tb * TB + t;
-      int head = 0;
-      unsigned long long kth = 0ull;
-      for (int k = 0; k < K; ++k) {
-        const unsigned long long mine =
-            (lane < NW && head < K) ? lists[((int64_t)lane * TB + t) * kTopkMaxK + head] : 0ull;
-        unsigned long long best = mine;
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-          best = other > best ? other : best;
-        }
-        if (best != 0ull && mine == best) ++head;  // keys are unique: one owner
-        if (lane == 0 && trial < a.T)
-          tk.cand[((int64_t)trial * a.n_tiles + tile) * K + k] = best;
-        kth = best;
-      }
-      if (lane == 0 && trial < a.T && kth) atomicMax(tk.thr + trial, kth);
-    }
-    __syncthreads();  // lists and values free for the next item
-  }
-}
-
-// Per trial: the K best of its tiles' candidate keys (keys are unique per
-// bin, so the order is total), decoded to (bin, value); -1 = no maximum.
-__global__ void k_topk_merge(const unsigned long long* __restrict__ cand, int T, int n_lists,
-                             int K, int64_t* idx, float* val) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= T) return;
-  const unsigned long long* c = cand + (int64_t)warp * n_lists;
-  unsigned long long top[kTopkMaxK];
-#pragma unroll
-  for (int k = 0; k < kTopkMaxK; ++k) top[k] = 0ull;
-  for (int i = lane; i < n_lists; i += 32) {  // per-lane sorted top-K
-    unsigned long long x = __ldg(c + i);
-#pragma unroll
-    for (int k = 0; k < kTopkMaxK; ++k) {
-      if (k < K && x > top[k]) {
-        const unsigned long long y = top[k];
-        top[k] = x;
-        x = y;
-      }
-    }
-  }
-  int head = 0;
-  for (int k = 0; k < K; ++k) {
-    unsigned long long mine = 0ull;
-#pragma unroll
-    for (int j = 0; j < kTopkMaxK; ++j)
-      if (j == head) mine = top[j];
-    unsigned long long best = mine;
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-      best = other > best ? other : best;
-    }
-    if (best != 0ull && mine == best) ++head;
-    if (lane == 0) {
-      const bool ok = best != 0ull;
-      idx[(int64_t)warp * K + k] = ok ? (int64_t)(0xffffffffull - (best & 0xffffffffull)) : -1;
-      const uint32_t u = (uint32_t)(best >> 32);
-      val[(int64_t)warp * K + k] = ok ? __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u)
-                                      : 0.0f;
-    }
-  }
-}
-
 __global__ void k_decode_keys(const unsigned long long* keys, int T, int64_t* idx, float* val) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
@@ -1161,62 +701,6 @@ void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T, int64
                         float* val_d) {
   KTimer kt(ctx, "decode");
   k_decode_keys<<<(T + 255) / 256, 256, 0, ctx->stream>>>(keys_d, T, idx_d, val_d);
-  GH_LAUNCHED(ctx);
-}
-
-void launch_gather_topk(Ctx* ctx, Table* t, const void* spec_d, int T, int K,
-                        unsigned long long* cand_d, unsigned long long* thr_d) {
-  const Plan& pl = t->plan_topk;
-  if (!pl.built) fail(GH_ERUNTIME, "gather: top-K plan not built");
-  if (K < 1 || K > kTopkMaxK) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
-  GatherArgs a{};
-  a.spec = spec_d;
-  a.tiles = pl.tiles_d;
-  a.win = pl.win_d;
-  a.rows = pl.rows_d;
-  a.n_entries = pl.n_entries;
-  a.grid = t->grid;
-  a.G = t->G;
-  a.P = t->P;
-  a.p4 = pl.p4;
-  a.M = t->M;
-  a.T = T;
-  a.n_batches = (T + pl.tb - 1) / pl.tb;
-  a.n_tiles = pl.n_tiles;
-  TopkArgs tk{};
-  tk.K = K;
-  tk.cand = cand_d;
-  tk.thr = thr_d;
-  const size_t win_bytes = ((size_t)pl.max_rows * pl.tb * pl.esize + 127) / 128 * 128;
-  tk.vals_off = static_cast<unsigned>(win_bytes);
-  tk.lists_off = static_cast<unsigned>(win_bytes + (pl.vals_bytes + 127) / 128 * 128);
-  tk.bmax = pl.pick_blocks;
-  tk.pos = pl.pos_d;
-  const size_t pick = std::max<size_t>((size_t)kTopkNW * 8 * kTopkMaxK * 8,
-                                       (size_t)pl.tb * pl.pick_blocks * 8);
-  const size_t smem = tk.lists_off + pick;
-  auto go = [&](auto kern) {
-    GH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    const int64_t items = (int64_t)a.n_tiles * a.n_batches;
-    const unsigned blocks =
-        static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(items, ctx->num_sms)));
-    KTimer kt(ctx, "gather");
-    kern<<<blocks, kTopkNW * 32, smem, ctx->stream>>>(a, tk);
-    GH_LAUNCHED(ctx);
-  };
-  const int pq = pl.p4 / 4;
-  if (t->P == 16) go(k_gather_topk<16, 4>);
-  else if (pq <= 1) go(k_gather_topk<0, 1>);
-  else if (pq <= 4) go(k_gather_topk<0, 4>);
-  else if (pq <= 8) go(k_gather_topk<0, 8>);
-  else go(k_gather_topk<0, 16>);
-}
-
-void launch_topk_merge(Ctx* ctx, const unsigned long long* cand_d, int T, int n_lists, int K,
-                       int64_t* idx_d, float* val_d) {
-  KTimer kt(ctx, "merge");
-  k_topk_merge<<<(T + 7) / 8, 256, 0, ctx->stream>>>(cand_d, T, n_lists, K, idx_d, val_d);
   GH_LAUNCHED(ctx);
 }
 

@@ -63,6 +63,7 @@ struct Ctx {
   size_t smem_optin = 227 * 1024;
   Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2, flagbuf;
   int twiddle_m = 0;
+  int topk_impl = 0;    // 0: auto, 1: fused gather + pick, 2: map then pick
   int direct_impl = 0;  // 0: tcgen05 3xFP16, 1: CUDA-core fp32, 2: tcgen05 v1, 3: tcgen05 3xTF32
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
   cudaStream_t copy_stream = nullptr;
@@ -139,10 +140,15 @@ struct TileDesc {
   int32_t cx0, cy0, cz0, cwx, cwy, cwz;
 };
 
-// values buffer pitch (bins) of a top-K tile row: == 2 mod 4, so the 32-byte
-// rows of a 2 x 4 block's upper and lower bin pairs fall in opposite halves of
-// the shared-memory banks
-__host__ __device__ __forceinline__ int topk_pitch(int wx) { return wx + ((6 - wx % 4) % 4); }
+// values plane pitch (floats) of a top-K tile row: >= wx + 2 (the box plus
+// its -inf ring) and == 4 mod 8, so the 4 x 4 positions of a gather step (two
+// 2 x 4 entry blocks) store to 16 distinct banks (y * pitch mod 32 =
+// 4 * (odd * y mod 8)) and rows stay 16-byte aligned for the LDS.128 filter
+__host__ __device__ __forceinline__ int topk_pitch(int wx) {
+  return wx + 2 + ((12 - (wx + 2) % 8) % 8);
+}
+// fused top-K: the kernel's static shared memory (candidate lists, band maxima)
+constexpr size_t kTopkListBytes = 8 * 1024;
 
 // Local entry lb of a tile -> tile coordinates. Plain tiles run x-fastest;
 // blocked tiles (8-trial power argmax plans) run 8-bin blocks (2 x 4 x 1 on
@@ -186,8 +192,8 @@ struct Plan {
   int64_t n_entries = 0;
   // top-K plans (halo tiles): per-tile values buffer in shared memory
   bool halo = false;
-  size_t vals_bytes = 0;   // the largest tile's [pitch * wy * wz][tb] fp32 values
-  int pick_blocks = 0;     // the largest tile's 4 x 4 core blocks (prune seeds)
+  size_t vals_bytes = 0;   // [tb trial planes][topk_plane] fp32 values
+  int topk_plane = 0;      // floats per trial plane (>= the largest tile's pitch * (wy + 2))
   uint16_t* pos_d = nullptr;  // [entries] values-buffer position of each entry
 };
 

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 
@@ -257,16 +258,19 @@ __global__ void k_fit_atoms(int n_samples, int os, const double* r, int n, int s
   }
 }
 
-// top-K plans: each entry's position in its tile's values buffer
-// ((lz * wy + ly) * pitch + lx), so the gather stores without decoding the
-// blocked entry order
+// top-K plans: each entry's position in its tile's values plane
+// ((ly + 1) * pitch + lx + 1, inside the -inf ring), bit 15 set for halo bins,
+// so the gather stores and tracks core maxima without decoding the blocked
+// entry order (2-D tiles)
 __global__ void k_fill_pos(const TileDesc* tiles, uint16_t* pos) {
   const TileDesc td = tiles[blockIdx.x];
   const int nb = td.wx * td.wy * td.wz, pitch = topk_pitch(td.wx);
   for (int lb = threadIdx.x; lb < nb; lb += blockDim.x) {
     int64_t lx, ly, lz;
     tile_local(td, lb, &lx, &ly, &lz);
-    pos[td.entry_off + lb] = static_cast<uint16_t>((lz * td.wy + ly) * pitch + lx);
+    const bool halo = lx < td.cx0 || lx >= td.cx0 + td.cwx || ly < td.cy0 || ly >= td.cy0 + td.cwy;
+    pos[td.entry_off + lb] =
+        static_cast<uint16_t>(((ly + 1) * pitch + lx + 1) | (halo ? 0x8000 : 0));
   }
 }
 
@@ -827,12 +831,7 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
 // shared memory next to the range windows (gh_gather.cu k_gather_topk).
 // Windows + values must share one CTA's shared memory, so tiles are smaller
 // than the argmax plan's (~56 x 56 bins on c3 instead of ~113 x 113).
-constexpr size_t kTopkSmem = 224 * 1024;  // windows + values + per-warp lists
-constexpr size_t kTopkLists = 24 * 8 * 8 * sizeof(unsigned long long);
-// the pick region first holds each trial's verified 4 x 4 block maxima
-inline size_t topk_pick_bytes(int blocks) {
-  return std::max<size_t>(kTopkLists, (size_t)8 * blocks * sizeof(unsigned long long));
-}
+constexpr size_t kTopkSmem = 224 * 1024;  // windows + values + lists, per SM
 
 Plan* build_plan_topk(Ctx* ctx, Table* t) {
   Plan& pl = t->plan_topk;
@@ -860,7 +859,7 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
     int max_rows = 0;
     int64_t entries = 0;
     size_t vals = 0;
-    int blocks = 0;
+    int plane = 0;
   };
   int2* mm_d = nullptr;
   TileDesc* tiles_d = nullptr;
@@ -892,11 +891,15 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
         td.entry_off = off;
         td.blk = td.wx % 2 == 0 && td.wy % 4 == 0 ? 1 + 1 + (2 << 2) : 0;  // 2 x 4 x 1
         off += (int64_t)td.wx * td.wy;
-        tl.vals = std::max(tl.vals, (size_t)topk_pitch(td.wx) * td.wy * 8 * sizeof(float));
-        tl.blocks = std::max(tl.blocks, ((td.cwx + 3) / 4) * ((td.cwy + 3) / 4));
+        tl.plane = std::max(tl.plane, topk_pitch(td.wx) * (td.wy + 2));
         tl.tiles.push_back(td);
       }
     tl.entries = off;
+    // trial planes 4 mod 8 floats apart: a gather store's two 4-trial lane
+    // halves land in opposite bank halves (+8: the filter's last float4 may
+    // run past the ring row)
+    tl.plane = (tl.plane + 8 + 3) / 8 * 8 + 4;
+    tl.vals = (size_t)tl.plane * 8 * sizeof(float);
     const size_t nt = tl.tiles.size();
     if (nt > tiles_cap) {
       if (tiles_d) cudaFree(tiles_d);
@@ -937,14 +940,16 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
     return tl;
   };
   auto smem_of = [&](const Tiling& tl) {
-    return ((size_t)tl.max_rows * 8 * 4 + 127) / 128 * 128 + (tl.vals + 127) / 128 * 128 +
-           topk_pick_bytes(tl.blocks);
+    // windows + two values buffers (the pick of one item overlaps the next
+    // item's gather) + the kernel's static lists
+    return ((size_t)tl.max_rows * 8 * 4 + 127) / 128 * 128 + 2 * ((tl.vals + 127) / 128 * 128) +
+           kTopkListBytes;
   };
   auto fits = [&](const Tiling& tl) {
     return smem_of(tl) <= kTopkSmem && tl.max_rows * 2 <= 65535;  // 16-byte units, L = 2
   };
   // start near values ~ 45 % of the budget, then shrink / grow the core
-  int w = static_cast<int>(std::sqrt(0.45 * kTopkSmem / 32.0)) - 3;
+  int w = static_cast<int>(std::sqrt(0.45 * kTopkSmem / 64.0)) - 3;
   w = std::max(4, std::min(w, std::max(g.n[0], g.n[1])));
   Tiling best = try_tiling(w);
   for (int i = 0; i < 40 && !fits(best) && w > 4; ++i) {
@@ -977,7 +982,7 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
   pl.max_rows = best.max_rows;
   pl.n_entries = best.entries;
   pl.vals_bytes = best.vals;
-  pl.pick_blocks = best.blocks;
+  pl.topk_plane = best.plane;
   GH_CUDA(cudaMalloc(&pl.rows_d, sizeof(uint16_t) * pl.n_entries * pl.p4));
   GH_CUDA(cudaMemsetAsync(pl.rows_d, 0, sizeof(uint16_t) * pl.n_entries * pl.p4, ctx->stream));
   int* err_d = nullptr;
@@ -1003,7 +1008,7 @@ Plan* build_plan_topk(Ctx* ctx, Table* t) {
   f.err = err_d;
   k_fill_plan<<<pl.n_tiles, 256, 0, ctx->stream>>>(f);
   GH_LAUNCHED(ctx);
-  if (best.vals / (8 * sizeof(float)) > 65535) fail(GH_EINVAL, "gather plan: top-K tile too large");
+  if (best.plane >= 0x8000) fail(GH_EINVAL, "gather plan: top-K tile too large");
   GH_CUDA(cudaMalloc(&pl.pos_d, sizeof(uint16_t) * pl.n_entries));
   k_fill_pos<<<pl.n_tiles, 256, 0, ctx->stream>>>(pl.tiles_d, pl.pos_d);
   GH_LAUNCHED(ctx);

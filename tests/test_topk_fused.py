@@ -22,6 +22,14 @@ from test_gpu_parity import frames_to_dev, topk_parity
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def fused_engine(ctx):
+    # these tests pin the fused engine; the session context is shared
+    ctx.set_topk_impl("fused")
+    yield
+    ctx.set_topk_impl("auto")
+
+
 def c3_sub(nx=240, ny=202):
     # BASELINE c3 stations / waveform (16 pairs, N = 1024, M = 4096) on a
     # sub-grid: a tiled table, so the fused plan applies
@@ -92,3 +100,17 @@ def test_fused_c3_full_grid_vs_unfused(ctx):
     ui, uv = unfused(ctx, sc, t, fd, k)
     assert np.array_equal(fi.cpu().numpy(), ui.cpu().numpy())
     assert np.array_equal(fv.cpu().numpy(), uv.cpu().numpy())
+
+
+def test_topk_engines_agree_on_a_ragged_batch(ctx):
+    # the 'map' engine through the same entry point: identical bins/values
+    sc = c3_sub(130, 114)
+    T, k = 13, 6
+    t = gh.precompute_hop_table(ctx, sc)
+    fr, _ = O.synth(sc, 3, T)
+    fd = frames_to_dev(fr)
+    fi, fv = gh.hop_topk(ctx, t, fd, k)
+    ctx.set_topk_impl("map")
+    mi, mv = gh.hop_topk(ctx, t, fd, k)
+    assert np.array_equal(fi.cpu().numpy(), mi.cpu().numpy())
+    assert np.array_equal(fv.cpu().numpy(), mv.cpu().numpy())
