@@ -1616,10 +1616,11 @@ int gh_fit_atom(gh_ctx* ctx, int32_t n_samples, int32_t os_range, const double* 
     gh::Buffer buf;
     auto* base = static_cast<unsigned char*>(
         buf.get(sizeof(double) * n + sizeof(uint32_t) * 3 * n + sizeof(double2) * 3 * n + sizeof(double) * n));
-    auto* rd = reinterpret_cast<double*>(base);
-    auto* cd = reinterpret_cast<double2*>(base + sizeof(double) * n);
-    auto* res = reinterpret_cast<double*>(base + sizeof(double) * n + sizeof(double2) * 3 * n);
-    auto* id = reinterpret_cast<uint32_t*>(base + 2 * sizeof(double) * n + sizeof(double2) * 3 * n);
+    // double2 first: every sub-array stays aligned for any n
+    auto* cd = reinterpret_cast<double2*>(base);
+    auto* rd = reinterpret_cast<double*>(base + sizeof(double2) * 3 * n);
+    auto* res = reinterpret_cast<double*>(base + sizeof(double2) * 3 * n + sizeof(double) * n);
+    auto* id = reinterpret_cast<uint32_t*>(base + sizeof(double2) * 3 * n + 2 * sizeof(double) * n);
     GH_CUDA(cudaMemcpyAsync(rd, r, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
     gh::launch_fit_atoms(c, n_samples, os_range, rd, n, scheme, id, cd, res);
     GH_CUDA(cudaMemcpyAsync(idx, id, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, c->stream));

@@ -80,7 +80,7 @@ int main() {
                                                                      frames.begin() + P * s.n_samples),
                                                static_cast<int>(hop.bin[0]));
   std::printf("{\"map_peak_t0\": %.9g, \"single_bin_t0\": %.9g}\n", map[size_t(hop.bin[0])], one);
-  const auto spec = gb::fast_time_spectra(ctx, frames, 1, P, s.n_samples, s.os_range);
+  const auto spec = gb::fast_time_spectra(ctx, frames, T, P, s.n_samples, s.os_range);
   std::printf("{\"spectrum_t0_p0_b0\": [%.9g, %.9g]}\n", spec[0].real(), spec[0].imag());
   // noise on noiseless frames equals the synthesis' own noise draws
   gb::SceneModel quiet = model;
