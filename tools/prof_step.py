@@ -24,6 +24,7 @@ def main():
     sc = S.baseline(a.config)
     T = a.trials or sc.trials
     ctx = gh.Context(0)
+    ctx.set_topk_impl("fused" if a.path == "topk" else "auto")
     table = gh.precompute_hop_table(ctx, sc) if a.path != "direct" else None
     frames, _ = gh.synthesize(ctx, sc, 0, T)
     for _ in range(a.steps):

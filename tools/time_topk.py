@@ -23,6 +23,7 @@ def main():
     a = ap.parse_args()
     sc = S.baseline(a.config)
     ctx = gh.Context(0)
+    ctx.set_topk_impl("fused")
     table = gh.precompute_hop_table(ctx, sc)
     fr, _ = gh.synthesize(ctx, sc, 0, a.trials)
     ctx.synchronize()
@@ -48,6 +49,7 @@ def main():
         return out
 
     fi, fv = timed("fused", lambda: gh.hop_topk(ctx, table, fr, sc.topk))
+    ctx.set_topk_impl("map")
     ui, uv = timed("map+pick", lambda: gh.topk_local_max(ctx, sc, gh.hop_decision_map(ctx, table, fr),
                                                         sc.topk))
     print("same idx:", bool(torch.equal(fi, ui)), "same val:", bool(torch.equal(fv, uv)))

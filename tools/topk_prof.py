@@ -21,6 +21,7 @@ def main():
     T = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
     sc = S.baseline("c3")
     ctx = gh.Context(0)
+    ctx.set_topk_impl("fused")
     table = gh.precompute_hop_table(ctx, sc)
     fr, _ = gh.synthesize(ctx, sc, 0, T)
     gh.hop_topk(ctx, table, fr, sc.topk)
