@@ -143,6 +143,10 @@ int gh_table_info(const gh_table* t, int64_t* n_bins, int32_t* n_pairs,
                   int32_t* k, int32_t* n_fft, double* max_residual);
 /* Copy the operator back in the reference layout (host pointers). */
 int gh_table_download(gh_table* t, uint32_t* idx, double* coef);
+/* Rows of a subset of the table's (global) bins, the layout of
+ * gh_table_download: idx [n][P][K], coef [n][P][K] (re, im) — spot checks of
+ * tables too large to download (BASELINE c5: 16.7M bins x 64 pairs). */
+int gh_table_rows(gh_table* table, const int64_t* bins, int64_t n, uint32_t* idx, double* coef);
 int gh_table_destroy(gh_table* t);
 
 /* ---- MRF1 capture container ---------------------------------------------

@@ -703,6 +703,66 @@ int or_build_table(const or_wave* w, const or_grid* g, int scheme, int wrap,
   });
 }
 
+int or_table_rows(const or_wave* w, const or_grid* g, int scheme, const int64_t* bins,
+                  int64_t n, int n_threads, uint32_t* idx, double* coef) {
+  return guarded([&] {
+    check_wave(*w);
+    const int K = scheme_order(scheme);
+    const int64_t G = grid_size(*g);
+    const int P = w->n_pairs;
+    for (int64_t i = 0; i < n; ++i)
+      if (bins[i] < 0 || bins[i] >= G) throw std::invalid_argument("table rows: bin out of range");
+    parallel_for(n, n_threads, [&](int64_t i) {
+      const int64_t b = bins[i];
+      double xb[3];
+      grid_point(*g, b, xb);
+      for (int p = 0; p < P; ++p) {
+        const double r = sensed_range(w->range_scale, w->tx + 3 * p, w->rx + 3 * p, xb);
+        const Fit f = fit_atom(w->n_samples, w->os_range, r, scheme);
+        const size_t at = (static_cast<size_t>(i) * P + p) * K;
+        for (int j = 0; j < K; ++j) {
+          idx[at + j] = f.idx[j];
+          coef[2 * (at + j)] = f.c[j].real();
+          coef[2 * (at + j) + 1] = f.c[j].imag();
+        }
+      }
+    });
+  });
+}
+
+int or_hop_map_onfly(const double* spectra, int32_t n_trials, const or_wave* w,
+                     const or_grid* g, int scheme, int magnitude, int n_threads, double* map) {
+  return guarded([&] {
+    check_wave(*w);
+    const int K = scheme_order(scheme);
+    const int64_t G = grid_size(*g);
+    const int P = w->n_pairs, M = w->n_samples * w->os_range;
+    const auto* sp = reinterpret_cast<const cplx*>(spectra);
+    constexpr int64_t kChunk = 1024;  // hopping.cpp:15
+    parallel_for((G + kChunk - 1) / kChunk, n_threads, [&](int64_t ch) {
+      std::vector<uint32_t> idx(static_cast<size_t>(P) * K);
+      std::vector<double> coef(static_cast<size_t>(P) * K * 2);
+      const int64_t b1 = std::min(G, (ch + 1) * kChunk);
+      for (int64_t b = ch * kChunk; b < b1; ++b) {
+        double xb[3];
+        grid_point(*g, b, xb);
+        for (int p = 0; p < P; ++p) {
+          const double r = sensed_range(w->range_scale, w->tx + 3 * p, w->rx + 3 * p, xb);
+          const Fit f = fit_atom(w->n_samples, w->os_range, r, scheme);
+          for (int j = 0; j < K; ++j) {
+            idx[static_cast<size_t>(p) * K + j] = f.idx[j];
+            coef[2 * (static_cast<size_t>(p) * K + j)] = f.c[j].real();
+            coef[2 * (static_cast<size_t>(p) * K + j) + 1] = f.c[j].imag();
+          }
+        }
+        for (int32_t t = 0; t < n_trials; ++t)  // one bin of each trial's map
+          hop_map_trial(sp + static_cast<size_t>(t) * P * M, P, M, idx.data(), coef.data(), 1, K,
+                        magnitude, map + static_cast<size_t>(t) * G + b);
+      }
+    });
+  });
+}
+
 int or_scene_sample(const or_wave* w, const or_campaign* c, uint64_t trial,
                     double* targets, double* alpha, double* sigma) {
   return guarded([&] {

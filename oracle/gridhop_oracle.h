@@ -85,6 +85,17 @@ int or_build_table(const or_wave* w, const or_grid* g, int scheme, int wrap,
                    int n_threads, uint32_t* idx, double* coef,
                    double* max_residual);
 
+/* Rows of the mapping operator for a subset of bins (or_build_table's
+ * per-entry fit, interp.cpp:156-223), wrap mode: idx [n][P][K], coef
+ * [n][P][K][2]. For grids too large to tabulate on the host (c5). */
+int or_table_rows(const or_wave* w, const or_grid* g, int scheme, const int64_t* bins,
+                  int64_t n, int n_threads, uint32_t* idx, double* coef);
+/* The hop map (hop_map_trial's arithmetic, hopping.cpp:59-102) with every
+ * (bin, pair) fitted on the fly instead of read from a stored table, bins
+ * parallel over threads: spectra [T][P][M][2] -> map [T][G]. */
+int or_hop_map_onfly(const double* spectra, int32_t n_trials, const or_wave* w,
+                     const or_grid* g, int scheme, int magnitude, int n_threads, double* map);
+
 int or_scene_sample(const or_wave* w, const or_campaign* c, uint64_t trial,
                     double* targets /*[K][3]*/, double* alpha /*[K][P][2]*/,
                     double* sigma /*[P]*/);

@@ -55,6 +55,9 @@ def lib():
             "or_spectra": (C.c_int, [vp, i64, i32, i32, vp]),
             "or_hop_map": (C.c_int, [vp, i32, i32, i32, vp, vp, i64, i32, C.c_int, vp]),
             "or_direct_map": (C.c_int, [vp, i32, P(CWave), P(CGrid), C.c_int, C.c_int, vp]),
+            "or_table_rows": (C.c_int, [P(CWave), P(CGrid), C.c_int, vp, i64, C.c_int, vp, vp]),
+            "or_hop_map_onfly": (C.c_int, [vp, i32, P(CWave), P(CGrid), C.c_int, C.c_int, C.c_int,
+                                           vp]),
             "or_argmax": (i64, [vp, i64]),
             "or_topk_local_max": (C.c_int, [vp, P(CGrid), i32, vp, vp]),
             "or_range_peaks": (C.c_int, [vp, i64, i32, i32, vp]),
@@ -196,6 +199,31 @@ def velocity(scene, frames: np.ndarray, loc: np.ndarray, doppler_scale: float, s
                                         doppler_scale, spacing, half, loc.ctypes.data,
                                         vidx.ctypes.data, vval.ctypes.data))
     return vidx, vval
+
+
+def table_rows(scene, bins: np.ndarray, scheme: int | None = None, threads: int | None = None):
+    """or_table_rows: the mapping operator's rows for a subset of bins."""
+    bins = np.ascontiguousarray(bins, dtype=np.int64)
+    K = lib().or_scheme_order(scene.scheme if scheme is None else scheme)
+    idx = np.zeros((bins.size, scene.n_pairs, K), dtype=np.uint32)
+    coef = np.zeros((bins.size, scene.n_pairs, K), dtype=np.complex128)
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().or_table_rows(C.byref(w), C.byref(g), scene.scheme if scheme is None else scheme,
+                               bins.ctypes.data, bins.size, threads or nthreads(), idx.ctypes.data,
+                               coef.ctypes.data))
+    return idx, coef
+
+
+def hop_map_onfly(scene, spec: np.ndarray, magnitude: bool = False, threads: int | None = None):
+    """or_hop_map_onfly: the hop map without a stored table (grids too large
+    to tabulate on the host): complex spectra [T, P, M] -> [T, G]."""
+    spec = np.ascontiguousarray(spec, dtype=np.complex128)
+    T = spec.shape[0]
+    out = np.zeros((T, scene.n_bins))
+    w, g = scene.c_wave(), scene.c_grid()
+    _check(lib().or_hop_map_onfly(spec.ctypes.data, T, C.byref(w), C.byref(g), scene.scheme,
+                                  int(magnitude), threads or nthreads(), out.ctypes.data))
+    return out
 
 
 def direct_map(scene, frames: np.ndarray, magnitude: bool = False, threads: int | None = None):

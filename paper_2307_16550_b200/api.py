@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
             "gh_table_build_shard": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, i32, i32, P(vp)]),
             "gh_table_info": (C.c_int, [vp, P(i64), P(i32), P(i32), P(i32), P(f64)]),
             "gh_table_download": (C.c_int, [vp, vp, vp]),
+            "gh_table_rows": (C.c_int, [vp, vp, i64, vp, vp]),
             "gh_table_destroy": (C.c_int, [vp]),
             "gh_synth_d": (C.c_int, [vp, P(CWave), P(CCampaign), u64, i32, i32, vp, vp]),
             "gh_spectra_d": (C.c_int, [vp, vp, i32, i32, i32, i32, vp]),
@@ -304,6 +305,15 @@ class HopTable:
             self.close()
         except Exception:
             pass
+
+    def rows(self, bins):
+        """(idx [n, P, K] uint32, coef [n, P, K] complex128) of the given global bins."""
+        bins = np.ascontiguousarray(bins, dtype=np.int64)
+        idx = np.zeros((bins.size, self.n_pairs, self.k), dtype=np.uint32)
+        coef = np.zeros((bins.size, self.n_pairs, self.k), dtype=np.complex128)
+        _check(lib().gh_table_rows(self.h, bins.ctypes.data, bins.size, idx.ctypes.data,
+                                   coef.ctypes.data))
+        return idx, coef
 
     def download(self):
         """(indices uint32 [G,P,K], coeffs complex128 [G,P,K]) in the reference layout."""

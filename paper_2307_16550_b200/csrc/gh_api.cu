@@ -878,6 +878,45 @@ int gh_table_download(gh_table* table, uint32_t* idx, double* coef) {
   });
 }
 
+// rows of a subset of (global) bins: idx [n][P][K], coef [n][P][K] (re, im)
+__global__ void k_table_rows(const uint32_t* idx_d, const double2* coef_d, const int64_t* bins,
+                             int64_t n, int64_t bin0, int PK, uint32_t* idx_o, double2* coef_o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * PK;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / PK, e = i - r * PK;
+    const int64_t src = (bins[r] - bin0) * PK + e;
+    idx_o[i] = idx_d[src];
+    coef_o[i] = coef_d ? coef_d[src] : make_double2(1.0, 0.0);  // nearest: unit (interp.cpp:92)
+  }
+}
+
+int gh_table_rows(gh_table* table, const int64_t* bins, int64_t n, uint32_t* idx, double* coef) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!t || (n > 0 && (!bins || !idx || !coef))) fail(GH_EINVAL, "hop table: null argument");
+    if (n < 0) fail(GH_EINVAL, "hop table: negative row count");
+    for (int64_t i = 0; i < n; ++i)
+      if (bins[i] < t->bin0 || bins[i] >= t->bin0 + t->G) fail(GH_EINVAL, "hop table: bin out of range");
+    if (n == 0) return;
+    gh::Ctx* c = t->ctx;
+    use_device(c);
+    const int PK = t->P * t->K;
+    gh::Buffer buf;
+    auto* base = static_cast<unsigned char*>(
+        buf.get(sizeof(double2) * n * PK + sizeof(int64_t) * n + sizeof(uint32_t) * n * PK));
+    auto* co = reinterpret_cast<double2*>(base);
+    auto* bd = reinterpret_cast<int64_t*>(base + sizeof(double2) * n * PK);
+    auto* io = reinterpret_cast<uint32_t*>(base + sizeof(double2) * n * PK + sizeof(int64_t) * n);
+    GH_CUDA(cudaMemcpyAsync(bd, bins, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    k_table_rows<<<grid_blocks(n * PK), 256, 0, c->stream>>>(t->idx_d, t->coef_d, bd, n, t->bin0, PK,
+                                                             io, co);
+    GH_LAUNCHED(c);
+    GH_CUDA(cudaMemcpyAsync(idx, io, sizeof(uint32_t) * n * PK, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaMemcpyAsync(coef, co, sizeof(double2) * n * PK, cudaMemcpyDeviceToHost, c->stream));
+    GH_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int gh_table_destroy(gh_table* table) {
   return guarded([&] {
     auto* t = reinterpret_cast<gh::Table*>(table);

@@ -1,0 +1,162 @@
+"""Full-size GPU parity for the BASELINE configs the round-1 tests only
+sampled: c4 on the whole 500 x 500 grid across its -10..20 dB sweep, the
+whole c5 16.7M-bin 3-D grid, and the campaign statistics (hit ratios,
+RMSE, half-resolution hits, K-target assignment) of c2 hop + direct, the c4
+sweep and c3 top-5 against the fp64 oracle.
+
+Gates (BASELINE.json north_star): bins identical to the oracle except
+near-ties (oracle values within 1e-5 of the map maximum), maps within 1e-4
+relative, statistics identical to the oracle campaign's once near-tie trials
+take the device's choice (the only documented difference). Campaign
+references: run_monte_carlo / hit_ratio (src/montecarlo.cpp:99-190), the
+reference's hop-vs-direct comparison (proj/tests/acceptance.cpp:241-294).
+"""
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2307_16550_b200 as gh
+from paper_2307_16550_b200 import scene as S
+from oracle import oracle as O
+
+from test_gpu_parity import (MAP_TOL, TIE_TOL, assert_argmax_parity, frames_to_dev, near_tie,
+                             rel_map_err, topk_parity)
+
+pytestmark = pytest.mark.gpu
+
+NTH = 15  # default thresholds 0.2 .. 3.0 m (scenario.cpp:177-179)
+
+
+def hop_maps(spec, oi, oc, magnitude=False):
+    """O.hop_map over trial chunks on every host core (ctypes drops the GIL)."""
+    T = spec.shape[0]
+    n = max(1, min(T, O.nthreads()))
+    cuts = np.linspace(0, T, n + 1).astype(int)
+    with ThreadPoolExecutor(n) as ex:
+        parts = list(ex.map(lambda ab: O.hop_map(spec[ab[0]:ab[1]], oi, oc, magnitude),
+                            [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]))
+    return np.concatenate(parts, axis=0)
+
+
+def substitute_near_ties(ref_maps, ref_est, gpu_est):
+    """Oracle estimates with each near-tie trial taking the device's bin;
+    any other difference fails."""
+    est = ref_est.copy()
+    for t in np.flatnonzero(ref_est != gpu_est):
+        assert near_tie(ref_maps[t], int(ref_est[t]), int(gpu_est[t])), (
+            t, ref_est[t], gpu_est[t], ref_maps[t][ref_est[t]], ref_maps[t][gpu_est[t]])
+        est[t] = gpu_est[t]
+    return est
+
+
+def assert_cell_equals(cell, ref_stats):
+    """gh_campaign_run's device statistics against or_trial_stats."""
+    assert cell["estimates"] == int(ref_stats[0])
+    assert cell["hits"] == [float(x) for x in ref_stats[1:1 + NTH]]
+    assert cell["hits_half_res"] == ref_stats[2 + NTH]
+    for got, want in ((cell["sq_err_sum"], ref_stats[1 + NTH]), (cell["err_sum"], ref_stats[3 + NTH])):
+        assert abs(got - want) <= 1e-12 * max(1.0, abs(want)), (got, want)
+
+
+@pytest.mark.parametrize("scheme", [S.POLY3, S.POLAR])
+def test_c4_full_grid_snr_sweep(ctx, scheme):
+    sc = S.baseline("c4").with_(scheme=scheme)
+    T = 64
+    oi, oc, _ = O.build_table(sc)
+    t = gh.precompute_hop_table(ctx, sc)
+    gi_, gc_ = t.download()
+    assert np.array_equal(gi_, oi) and np.abs(gc_ - oc).max() < 1e-9
+    snrs = list(sc.snr_sweep)
+    cells = gh.campaign_run(ctx, sc, T, algorithms=("hop",), snr_db=snrs)
+    assert [c["snr_db"] for c in cells] == snrs
+    rmse = []
+    for snr, cell in zip(snrs, cells):
+        fr, truth = O.synth(sc, 0, T, snr_db=snr)
+        ref = hop_maps(O.spectra(fr, sc.n_fft), oi, oc)
+        ref_est = np.argmax(ref, axis=1)
+        # frames-in: bins and maps against the oracle on the same frames
+        fd = frames_to_dev(fr)
+        g_idx = gh.hop_argmax(ctx, t, fd)[0].cpu().numpy()
+        assert_argmax_parity(ref, g_idx, f"c4 scheme {scheme} {snr} dB")
+        m = gh.hop_decision_map(ctx, t, fd[:4]).cpu().numpy()
+        assert rel_map_err(m, ref[:4]) < MAP_TOL
+        # the campaign (synthesis fused into the FFT): its statistics are the
+        # oracle campaign's up to near-tie trials
+        c_idx = gh.campaign_hop(ctx, t, sc, 0, T, snr_db=snr)[0].cpu().numpy()
+        est = substitute_near_ties(ref, ref_est, c_idx)
+        ref_stats, _ = O.trial_stats(sc, est, truth)
+        assert_cell_equals(cell, ref_stats)
+        rmse.append(cell["rmse_m"])
+    # an RMSE curve that falls with SNR (-10 dB vs 20 dB)
+    assert rmse[-1] < rmse[0]
+
+
+def test_c5_full_grid_table_sample_map_and_peaks(ctx):
+    sc = S.baseline("c5")
+    assert sc.n_bins == 512 * 512 * 64
+    t = gh.precompute_hop_table(ctx, sc)
+    rng = np.random.default_rng(20260816)
+    bins = np.sort(rng.choice(sc.n_bins, size=100_000, replace=False))
+    bins[:2] = (0, sc.n_bins - 1)
+    gi_, gc_ = t.rows(bins)
+    oi, oc = O.table_rows(sc, bins)
+    assert np.array_equal(gi_, oi)
+    assert np.abs(gc_ - oc).max() < 1e-12
+    T = 2
+    fr, _ = O.synth(sc, 0, T)
+    ref = O.hop_map_onfly(sc, O.spectra(fr, sc.n_fft))
+    fd = frames_to_dev(fr)
+    m = gh.hop_decision_map(ctx, t, fd).cpu().numpy()
+    assert rel_map_err(m, ref) < MAP_TOL
+    assert_argmax_parity(ref, gh.hop_argmax(ctx, t, fd)[0].cpu().numpy(), "c5 full grid")
+    # the 3 targets: top-3 local maxima over the 26-neighbourhood
+    topk_parity(ref, gh.hop_topk(ctx, t, fd, sc.topk)[0].cpu().numpy(), sc, sc.topk, "c5 top-3")
+
+
+def test_c2_hop_and_direct_statistics(ctx):
+    # BASELINE c2 "run both ways": per-trial argmax, RMSE and the fraction
+    # within 1 m for the direct method and grid hopping (>= 1000 trials)
+    sc = S.baseline("c2")
+    T = 1000
+    oi, oc, _ = O.build_table(sc)
+    t = gh.precompute_hop_table(ctx, sc)
+    fr, truth = O.synth(sc, 0, T)
+    ref_hop = hop_maps(O.spectra(fr, sc.n_fft), oi, oc)
+    ref_dir = O.direct_map(sc, fr)
+    cells = {c["algorithm"]: c for c in gh.campaign_run(ctx, sc, T, algorithms=("hop", "direct"))}
+    c_hop = gh.campaign_hop(ctx, t, sc, 0, T)[0].cpu().numpy()
+    g_fr, _ = gh.synthesize(ctx, sc, 0, T)
+    c_dir = gh.direct_argmax(ctx, sc, g_fr)[0].cpu().numpy()
+    for name, ref, g in (("hop", ref_hop, c_hop), ("direct", ref_dir, c_dir)):
+        est = substitute_near_ties(ref, np.argmax(ref, axis=1), g)
+        ref_stats, _ = O.trial_stats(sc, est, truth)
+        assert_cell_equals(cells[name], ref_stats)
+    # the reference's ordering claim on this scene: the direct method is at
+    # least as accurate as nearest-bin grid hopping (acceptance.cpp:241-294)
+    within_1m = {k: c["hit_ratio"][4] for k, c in cells.items()}  # threshold 5 = 1.0 m
+    assert within_1m["direct"] >= within_1m["hop"] - 0.02, within_1m
+
+
+def test_c3_top5_assignment_statistics(ctx):
+    # BASELINE c3: K = 5 targets, top-5 local maxima; the K-target assignment
+    # statistics of the device campaign against the oracle's
+    sc = S.baseline("c3")
+    T = 48
+    oi, oc, _ = O.build_table(sc)
+    t = gh.precompute_hop_table(ctx, sc)
+    fr, truth = O.synth(sc, 0, T)
+    ref = hop_maps(O.spectra(fr, sc.n_fft), oi, oc)
+    cell = gh.campaign_run(ctx, sc, T, algorithms=("hop",))[0]
+    c_top = gh.campaign_hop_topk(ctx, t, sc, 0, T, sc.topk)[0].cpu().numpy()
+    topk_parity(ref, c_top, sc, sc.topk, "c3 campaign top-5")
+    est = np.stack([O.topk_local_max(sc, ref[k], sc.topk)[0] for k in range(T)])
+    for k in range(T):  # near-tie trials take the device's list
+        if not np.array_equal(est[k], c_top[k]):
+            est[k] = c_top[k]
+    ref_stats, assign = O.trial_stats(sc, est, truth)
+    assert cell["estimates"] == sc.topk * T
+    assert_cell_equals(cell, ref_stats)
+    assert (assign >= -1).all()
