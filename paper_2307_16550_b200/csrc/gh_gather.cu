@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
       const int64_t lb = blk + (!check || j < nblk ? j : 0);
       float2 acc[2];
       acc[0] = acc[1] = f2(0.f, 0.f);
-      const float2* cf = K3 ? a.coef3 + entry0 + lb : nullptr;
+      const float2* cf = K3 && a.coef3 ? a.coef3 + entry0 + lb : nullptr;
+      const float4* cr = K3 && a.coefr ? a.coefr + entry0 + lb : nullptr;
       if constexpr (CP) {
         const unsigned wd = __shfl_sync(0xffffffffu, cur[0].x, j & 31);
         const unsigned mask = (1u << a.cbits) - 1u;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
           const int p = 4 * q + u;
           if (PC ? p >= PC : p >= a.P) break;
           accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p * a.n_entries, acc, p == 0,
-                                     a.n_entries);
+                                     a.n_entries, cr ? cr + p * a.n_entries : nullptr);
         }
       }
       float vals[TPL];
@@ -450,7 +451,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
           if (s + 1 < SMAX && sb + (s + 1) * BPW < w1) load(s + 1, wn);
           const int lb = sb + s * BPW + sub;
           if (lb < w1) {
-            const float2* cf = K3 ? a.coef3 + entry0 + lb : nullptr;
+            const float2* cf = K3 && a.coef3 ? a.coef3 + entry0 + lb : nullptr;
+      const float4* cr = K3 && a.coefr ? a.coefr + entry0 + lb : nullptr;
 #pragma unroll
             for (int q = 0; q < CQ; ++q) {
               const unsigned o[4] = {wc[q].x & 0xffffu, wc[q].x >> 16, wc[q].y & 0xffffu,
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
                 const int p = c * CPP + 4 * q + u;
                 if (p >= P) break;
                 accumulate<TB, K3, MAG, L>(smv, o[u], cf + 3 * p * a.n_entries, acc[s], false,
-                                           a.n_entries);
+                                           a.n_entries, cr ? cr + p * a.n_entries : nullptr);
               }
             }
           }
@@ -659,6 +661,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.rows = pl.rows_d;
   a.n_entries = pl.n_entries;
   a.coef3 = pl.coef3_d;
+  a.coefr = pl.coefr_d;
   a.binid = pl.full ? pl.binid_d : nullptr;
   a.crow = pl.full ? pl.crow_d : nullptr;
   a.cbits = pl.cbits;

@@ -16,7 +16,8 @@ struct GatherArgs {
   const int4* win;        // [tiles][P] / [P]
   const uint16_t* rows;   // [p4 / 4][entries][4], 16-byte units (word-major)
   int64_t n_entries;      // entries of the plan (word stride of rows)
-  const float2* coef3;    // [P][3][entries] (word-major)
+  const float2* coef3;    // [P][3][entries] (word-major), complex weights (poly3, linear)
+  const float4* coefr;    // [P][entries] real weights (w0, w1, w2, 0): polar tables, else null
   const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
   const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
   int cbits;              // bits per ring row in crow
@@ -39,7 +40,8 @@ __device__ __forceinline__ float2 f2(float x, float y) { return make_float2(x, y
 template <int TB, bool K3, bool MAG, int L>
 __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsigned off16,
                                            const float2* __restrict__ cf, float2 (&acc)[2],
-                                           bool first, int64_t cs = 0) {
+                                           bool first, int64_t cs = 0,
+                                           const float4* __restrict__ cr = nullptr) {
   if constexpr (!K3) {
     const float4 z = smv[off16];
     if (first) {
@@ -50,23 +52,35 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
       acc[1] = __fadd2_rn(acc[1], f2(z.z, z.w));
     }
   } else {
-    const float2 c0 = __ldg(cf), c1 = __ldg(cf + cs), c2 = __ldg(cf + 2 * cs);
     const float4 z0 = smv[off16];
     const float4 z1 = smv[off16 + L];
     const float4 z2 = smv[off16 + 2 * L];
-    // trial a = (x, y), trial b = (z, w); v = sum_j c_j z_j (complex product)
-    float2 ra = __fmul2_rn(f2(c0.x, c0.x), f2(z0.x, z0.y));           // (c0r*zr, c0r*zi)
-    ra = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.y, z0.x), ra);              // (-c0i*zi, c0i*zr)
-    ra = __ffma2_rn(f2(c1.x, c1.x), f2(z1.x, z1.y), ra);
-    ra = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.y, z1.x), ra);
-    ra = __ffma2_rn(f2(c2.x, c2.x), f2(z2.x, z2.y), ra);
-    ra = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.y, z2.x), ra);
-    float2 rb = __fmul2_rn(f2(c0.x, c0.x), f2(z0.z, z0.w));
-    rb = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.w, z0.z), rb);
-    rb = __ffma2_rn(f2(c1.x, c1.x), f2(z1.z, z1.w), rb);
-    rb = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.w, z1.z), rb);
-    rb = __ffma2_rn(f2(c2.x, c2.x), f2(z2.z, z2.w), rb);
-    rb = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.w, z2.z), rb);
+    float2 ra, rb;
+    if (cr) {
+      // real weights (polar interpolation): one 16-byte load, 3 FFMA2 per trial
+      const float4 w = __ldg(cr);
+      ra = __fmul2_rn(f2(w.x, w.x), f2(z0.x, z0.y));
+      ra = __ffma2_rn(f2(w.y, w.y), f2(z1.x, z1.y), ra);
+      ra = __ffma2_rn(f2(w.z, w.z), f2(z2.x, z2.y), ra);
+      rb = __fmul2_rn(f2(w.x, w.x), f2(z0.z, z0.w));
+      rb = __ffma2_rn(f2(w.y, w.y), f2(z1.z, z1.w), rb);
+      rb = __ffma2_rn(f2(w.z, w.z), f2(z2.z, z2.w), rb);
+    } else {
+      const float2 c0 = __ldg(cf), c1 = __ldg(cf + cs), c2 = __ldg(cf + 2 * cs);
+      // trial a = (x, y), trial b = (z, w); v = sum_j c_j z_j (complex product)
+      ra = __fmul2_rn(f2(c0.x, c0.x), f2(z0.x, z0.y));           // (c0r*zr, c0r*zi)
+      ra = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.y, z0.x), ra);      // (-c0i*zi, c0i*zr)
+      ra = __ffma2_rn(f2(c1.x, c1.x), f2(z1.x, z1.y), ra);
+      ra = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.y, z1.x), ra);
+      ra = __ffma2_rn(f2(c2.x, c2.x), f2(z2.x, z2.y), ra);
+      ra = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.y, z2.x), ra);
+      rb = __fmul2_rn(f2(c0.x, c0.x), f2(z0.z, z0.w));
+      rb = __ffma2_rn(f2(-c0.y, c0.y), f2(z0.w, z0.z), rb);
+      rb = __ffma2_rn(f2(c1.x, c1.x), f2(z1.z, z1.w), rb);
+      rb = __ffma2_rn(f2(-c1.y, c1.y), f2(z1.w, z1.z), rb);
+      rb = __ffma2_rn(f2(c2.x, c2.x), f2(z2.z, z2.w), rb);
+      rb = __ffma2_rn(f2(-c2.y, c2.y), f2(z2.w, z2.z), rb);
+    }
     const float2 sq = __ffma2_rn(f2(ra.x, rb.x), f2(ra.x, rb.x),
                                  __fmul2_rn(f2(ra.y, rb.y), f2(ra.y, rb.y)));
     const float2 v = MAG ? f2(sqrtf(sq.x), sqrtf(sq.y)) : sq;

@@ -185,7 +185,8 @@ struct Plan {
   TileDesc* tiles_d = nullptr;   // tiled plan
   int4* win_d = nullptr;         // [tiles][P] {base, len, row_start, 0}
   uint16_t* rows_d = nullptr;    // [entries][p4] first staged row per pair
-  float2* coef3_d = nullptr;     // [entries][P][3] (k3 only)
+  float2* coef3_d = nullptr;     // [P][3][entries] complex weights (k3, complex schemes)
+  float4* coefr_d = nullptr;     // [P][entries] real weights (k3 polar tables), instead of coef3_d
   uint32_t* binid_d = nullptr;   // [entries] global bin of each entry (permuted plans)
   uint32_t* crow_d = nullptr;    // [entries] compact ring rows (cbits per pair), or null
   int cbits = 0;

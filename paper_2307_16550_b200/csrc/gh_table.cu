@@ -342,6 +342,7 @@ struct FillArgs {
   int64_t n_entries;      // plan entries: row words are stored [p / 4][entry]
   uint16_t* rows;
   float2* coef3;
+  float4* coefr;  // real weights (polar): [P][entries]
   int* err;
 };
 
@@ -379,7 +380,16 @@ __global__ void k_fill_plan(FillArgs a) {
     // word-major ([pair / 4][entry] of 4 x uint16): the gather's lanes load
     // one word of consecutive entries, i.e. contiguous 8-byte runs
     a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb) * 4 + (p & 3)] = (uint16_t)off16;
-    if (a.k3) {
+    if (a.k3 && a.coefr) {
+      // polar weights are real (the anchors' chords): 3 floats + pad, one
+      // 16-byte load per (bin, pair) in the gather, [pair][entry]
+      float w[3];
+      for (int j = 0; j < 3; ++j) {
+        w[j] = j < a.K ? (float)a.coef[at + j].x : 0.0f;
+        if (j < a.K && a.coef[at + j].y != 0.0) atomicOr(a.err, 4);
+      }
+      a.coefr[(int64_t)p * a.n_entries + entry0 + lb] = make_float4(w[0], w[1], w[2], 0.0f);
+    } else if (a.k3) {
       // word-major like the rows: [pair][j][entry]
       for (int j = 0; j < 3; ++j) {
         const double2 c = j < a.K ? a.coef[at + j] : make_double2(0.0, 0.0);
@@ -785,7 +795,9 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
   }
   GH_CUDA(cudaMalloc(&pl.rows_d, sizeof(uint16_t) * pl.n_entries * pl.p4));
   GH_CUDA(cudaMemsetAsync(pl.rows_d, 0, sizeof(uint16_t) * pl.n_entries * pl.p4, ctx->stream));
-  if (pl.k3) GH_CUDA(cudaMalloc(&pl.coef3_d, sizeof(float2) * pl.n_entries * P * 3));
+  const bool real_w = pl.k3 && t->scheme == GH_POLAR;  // polar coefficients are real
+  if (real_w) GH_CUDA(cudaMalloc(&pl.coefr_d, sizeof(float4) * pl.n_entries * P));
+  else if (pl.k3) GH_CUDA(cudaMalloc(&pl.coef3_d, sizeof(float2) * pl.n_entries * P * 3));
   FillArgs f{};
   f.tiles = pl.full ? nullptr : pl.tiles_d;
   f.grid = t->grid;
@@ -803,6 +815,7 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
   f.rows = pl.rows_d;
   f.n_entries = pl.n_entries;
   f.coef3 = pl.coef3_d;
+  f.coefr = pl.coefr_d;
   f.err = err_d;
   if (pl.full) {
     const int blocks = static_cast<int>(std::min<int64_t>((t->G * P + 255) / 256, 148LL * 32));
@@ -815,6 +828,7 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
   GH_CUDA(cudaMemcpyAsync(&herr, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   GH_CUDA(cudaStreamSynchronize(ctx->stream));
   cudaFree(err_d);
+  if (herr & 4) fail(GH_EINVAL, "hop table: polar coefficients must be real");
   if (herr) fail(GH_ERUNTIME, "gather plan: an index fell outside its staged window");
   if (pl.full && !pl.k3 && P <= 8) permute_for_banks(ctx, t, pl);
   pl.built = true;
