@@ -343,7 +343,8 @@ constexpr int tiled_smax() { return K3 ? 6 : 8; }
 template <int TB, int ES, int L, int CPP>
 __device__ __noinline__ void stage_chunk(const GatherArgs& a, int P, int64_t item, int c,
                                          unsigned char* smraw, uint64_t* bar) {
-  const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
+  int tile, tb;
+  item_tile_batch(a, item, &tile, &tb);
   const int4* win = a.win + (int64_t)tile * a.P;
   const uint4* spec = reinterpret_cast<const uint4*>(static_cast<const unsigned char*>(a.spec) +
                                                      (int64_t)tb * a.P * a.M * TB * ES);
@@ -410,7 +411,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_gather_tiled(GatherArgs a) {
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint32_t it = 0;
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-    const int tile = (int)(item % a.n_tiles), tb = (int)(item / a.n_tiles);
+    int tile, tb;
+  item_tile_batch(a, item, &tile, &tb);
     const TileDesc td = a.tiles[tile];
     const int64_t entry0 = td.entry_off;
     const int nb = td.wx * td.wy * td.wz;
@@ -678,6 +680,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.keys = keys_d;
   const int n_tb = (T + pl.tb - 1) / pl.tb;
   a.n_batches = n_tb;
+  a.batch_group = 8;  // 64 trials per pass over a tile's plan rows (8-trial batches)
   a.n_tiles = pl.n_tiles;
   a.chunk_pairs = pl.chunk_pairs;
   if (n_tb > 65535) fail(GH_EINVAL, "gather: too many trial batches for one launch");

@@ -26,6 +26,7 @@ struct GatherArgs {
   int64_t G;              // bins of the table (shard)
   int64_t bin0;           // global index of the shard's first bin
   int n_batches;          // trial batches (full plan: persistent work split)
+  int batch_group;        // persistent tiled gather: batches per group (items group-major)
   int n_tiles;            // tiled plan
   int chunk_pairs;        // tiled plan: pairs per staging chunk
   int full;
@@ -86,6 +87,28 @@ __device__ __forceinline__ void accumulate(const float4* __restrict__ smv, unsig
     const float2 v = MAG ? f2(sqrtf(sq.x), sqrtf(sq.y)) : sq;
     if (first) acc[0] = v;
     else acc[0] = __fadd2_rn(acc[0], v);
+  }
+}
+
+// Persistent tiled gathers walk items group-major: groups of `batch_group`
+// trial batches, and inside a group tile-major, so the plan rows of a tile
+// are read once per group (its batches run together on neighbouring CTAs:
+// L2 hits) while the group's spectra stay L2-resident. item -> (tile, batch).
+__device__ __forceinline__ void item_tile_batch(const GatherArgs& a, int64_t item, int* tile,
+                                                int* tb) {
+  const int bg = a.batch_group;
+  const int full = a.n_batches / bg;
+  const int64_t per_group = (int64_t)a.n_tiles * bg;
+  if (item < full * per_group) {
+    const int g = (int)(item / per_group);
+    const int r = (int)(item - g * per_group);
+    *tile = r / bg;
+    *tb = g * bg + r % bg;
+  } else {
+    const int bl = a.n_batches - full * bg;  // last, partial group
+    const int r = (int)(item - full * per_group);
+    *tile = r / bl;
+    *tb = full * bg + r % bl;
   }
 }
 
