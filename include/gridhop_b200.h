@@ -133,6 +133,13 @@ int gh_table_build(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
 int gh_table_build_shard(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid,
                          int32_t scheme, int32_t wrap, int32_t layer_lo,
                          int32_t layer_hi, gh_table** out);
+/* Halo shards for multi-target picks across location-grid shards: a shard
+ * built one layer beyond its core on each interior side reports top-k
+ * local maxima of the core layers [core_lo, core_hi) only (global layer
+ * indices inside the shard); the halo layers complete the neighbourhoods of
+ * the core's border bins, so per-shard candidates merge exactly (all-gather
+ * of K keys per trial, then the K best). */
+int gh_table_set_core(gh_table* table, int32_t core_lo, int32_t core_hi);
 /* load_hop_table (src/interp.cpp:318-389) analogue: host arrays in the
  * reference layout [bin][pair][K] (HopTable::entry_offset, interp.hpp:55-59);
  * coef = complex128 (re, im) pairs, NULL means all ones (K = 1). */

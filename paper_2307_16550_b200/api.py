@@ -147,6 +147,7 @@ def lib() -> C.CDLL:
             "gh_table_info": (C.c_int, [vp, P(i64), P(i32), P(i32), P(i32), P(f64)]),
             "gh_table_download": (C.c_int, [vp, vp, vp]),
             "gh_table_rows": (C.c_int, [vp, vp, i64, vp, vp]),
+            "gh_table_set_core": (C.c_int, [vp, i32, i32]),
             "gh_table_destroy": (C.c_int, [vp]),
             "gh_synth_d": (C.c_int, [vp, P(CWave), P(CCampaign), u64, i32, i32, vp, vp]),
             "gh_spectra_d": (C.c_int, [vp, vp, i32, i32, i32, i32, vp]),
@@ -337,17 +338,26 @@ def precompute_hop_table(ctx: Context, scene: Scene, scheme: int | None = None,
 
 
 def precompute_hop_table_shard(ctx: Context, scene: Scene, layer_lo: int, layer_hi: int,
-                               scheme: int | None = None, wrap: bool | None = None) -> HopTable:
+                               scheme: int | None = None, wrap: bool | None = None,
+                               halo: bool = False) -> HopTable:
     """Location-grid shard (BASELINE c5): the operator for layers [lo, hi) of
-    z (3-D) / y (2-D); reported bin indices are global."""
+    z (3-D) / y (2-D); reported bin indices are global. halo=True builds one
+    extra layer on each interior side and reports top-k peaks of [lo, hi)
+    only, so per-shard top-k candidates merge exactly (distributed.merge_topk);
+    maps and argmax then cover the halo layers too."""
+    n_layers = scene.slab_axis_len()
+    b_lo, b_hi = (max(0, layer_lo - 1), min(n_layers, layer_hi + 1)) if halo else (layer_lo, layer_hi)
     h = C.c_void_p()
     w, g = scene.c_wave(), scene.c_grid()
     _check(lib().gh_table_build_shard(ctx.h, C.byref(w), C.byref(g),
                                       scene.scheme if scheme is None else scheme,
-                                      int(scene.wrap if wrap is None else wrap), layer_lo, layer_hi,
+                                      int(scene.wrap if wrap is None else wrap), b_lo, b_hi,
                                       C.byref(h)))
     t = HopTable(ctx, scene, h)
-    t.bin0, _ = scene.slab_bins(layer_lo, layer_hi)
+    t.bin0, _ = scene.slab_bins(b_lo, b_hi)
+    t.core = (layer_lo, layer_hi)
+    if halo:
+        _check(lib().gh_table_set_core(h, layer_lo, layer_hi))
     return t
 
 

@@ -268,7 +268,13 @@ void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthPar
     gh_grid lg = t->grid;
     if (lg.n[2] > 1) lg.n[2] = t->slab_hi - t->slab_lo;
     else lg.n[1] = t->slab_hi - t->slab_lo;
-    gh::launch_topk(c, map, tc, lg, K, t->bin0, idx_d + (int64_t)t0 * K, val_d + (int64_t)t0 * K);
+    // halo shards report the peaks of their core layers only; the halo
+    // layers complete the border bins' neighbourhoods
+    const int64_t layer = (int64_t)lg.n[0] * (lg.n[2] > 1 ? lg.n[1] : 1);
+    const int64_t e0 = t->core_hi > t->core_lo ? (t->core_lo - t->slab_lo) * layer : 0;
+    const int64_t e1 = t->core_hi > t->core_lo ? (t->core_hi - t->slab_lo) * layer : -1;
+    gh::launch_topk(c, map, tc, lg, K, t->bin0, idx_d + (int64_t)t0 * K, val_d + (int64_t)t0 * K,
+                    e0, e1);
   }
 }
 
@@ -817,6 +823,17 @@ int gh_table_build_shard(gh_ctx* ctx, const gh_wave* wave, const gh_grid* grid, 
       throw;
     }
     *out = reinterpret_cast<gh_table*>(t);
+  });
+}
+
+int gh_table_set_core(gh_table* table, int32_t core_lo, int32_t core_hi) {
+  return guarded([&] {
+    auto* t = reinterpret_cast<gh::Table*>(table);
+    if (!t) fail(GH_EINVAL, "hop table: null argument");
+    if (core_lo < t->slab_lo || core_hi > t->slab_hi || core_lo >= core_hi)
+      fail(GH_EINVAL, "hop table: core layers outside the shard");
+    t->core_lo = core_lo;
+    t->core_hi = core_hi;
   });
 }
 

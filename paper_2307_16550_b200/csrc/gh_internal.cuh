@@ -204,6 +204,7 @@ struct Table {
   int64_t G = 0;              // bins of this table (a shard: layers [slab_lo, slab_hi))
   int64_t bin0 = 0;           // global index of the first bin (location-grid shard)
   int slab_lo = 0, slab_hi = 0;  // layer range along z (3-D) or y (2-D)
+  int core_lo = 0, core_hi = 0;  // layers whose peaks top-k reports (halo shards), 0/0: all
   int P = 0, N = 0, os = 1, M = 0;
   double scale = 0.0;
   gh_grid grid{};             // the FULL grid: points stay bit-identical
@@ -296,8 +297,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,
 void launch_decode_keys(Ctx* ctx, const unsigned long long* keys_d, int T,
                         int64_t* idx_d, float* val_d);
 void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
-                 int64_t* idx_d,
-                 float* val_d);
+                 int64_t* idx_d, float* val_d, int64_t e0 = 0, int64_t e1 = -1);
 // velocity stage (gh_velocity.cu): hop (Doppler spectrum lookups) or direct
 void launch_velocity(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_grid* g,
                      const gh_velocity_grid* vg, const float2* frames_d, int T, int Mc,

@@ -134,9 +134,12 @@ __device__ __forceinline__ void warp_offer(WarpTopK& w, unsigned long long* q,
   w.qn += __popc(pend);
 }
 
+// Candidates are the elements [e0, e1) of each trial's map (a shard's core
+// layers); neighbours are read over the whole map (its halo layers too).
 __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __restrict__ map,
                                                                int64_t G, int nx, int ny, int nz,
-                                                               int K, int64_t bin0, int64_t* idx_out,
+                                                               int K, int64_t bin0, int64_t e0,
+                                                               int64_t e1, int64_t* idx_out,
                                                                float* val_out) {
   constexpr int NW = kTopkThreads / 32;
   __shared__ unsigned long long cta_thr;
@@ -149,22 +152,25 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
   const int trial = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* m = map + (int64_t)trial * G;
+  const float* mc = m + e0;  // the scanned range
+  const int64_t Gc = e1 - e0;
   if (threadIdx.x == 0) cta_thr = 0ull;
   __syncthreads();
   WarpTopK w{0ull, 0, 0ull, 0};
   unsigned long long* wq = queue[warp];
   // scalar head up to 16-byte alignment, float4 body, scalar tail; loops
   // have warp-uniform trip counts (inactive lanes offer nothing)
-  const int64_t lead = (int64_t)((16 - (reinterpret_cast<uintptr_t>(m) & 15)) & 15) / 4;
-  const int64_t h = lead < G ? lead : G;
+  const int64_t lead = (int64_t)((16 - (reinterpret_cast<uintptr_t>(mc) & 15)) & 15) / 4;
+  const int64_t h = lead < Gc ? lead : Gc;
   for (int64_t b = 0; b < h; b += kTopkThreads) {
     const int64_t i = b + threadIdx.x;
     const bool act = i < h;
-    warp_offer(w, wq, m, act ? __ldg(m + i) : 0.f, (uint32_t)i, act, K, nx, ny, nz, &cta_thr);
+    warp_offer(w, wq, m, act ? __ldg(mc + i) : 0.f, (uint32_t)(e0 + i), act, K, nx, ny, nz,
+               &cta_thr);
     while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
   }
-  const float4* m4 = reinterpret_cast<const float4*>(m + h);
-  const int64_t n4 = (G - h) / 4;
+  const float4* m4 = reinterpret_cast<const float4*>(mc + h);
+  const int64_t n4 = (Gc - h) / 4;
   for (int64_t g0 = 0; g0 < n4; g0 += (int64_t)kTopkThreads * kVec) {
     float4 q[kVec];
 #pragma unroll
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
     for (int u = 0; u < kVec; ++u) {
       const int64_t g = g0 + (int64_t)u * kTopkThreads + threadIdx.x;
       const bool act = g < n4;
-      const uint32_t i = (uint32_t)(h + 4 * g);
+      const uint32_t i = (uint32_t)(e0 + h + 4 * g);
       // float pre-filter: key > prune key implies value >= its value, so a
       // float4 whose four values are all below it is skipped in one vote
       const float tv = w.thr ? unord(static_cast<uint32_t>(w.thr >> 32)) : -INFINITY;
@@ -191,10 +197,11 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
       while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
     }
   }
-  for (int64_t b = h + 4 * n4; b < G; b += kTopkThreads) {
+  for (int64_t b = h + 4 * n4; b < Gc; b += kTopkThreads) {
     const int64_t i = b + threadIdx.x;
-    const bool act = i < G;
-    warp_offer(w, wq, m, act ? __ldg(m + i) : 0.f, (uint32_t)i, act, K, nx, ny, nz, &cta_thr);
+    const bool act = i < Gc;
+    warp_offer(w, wq, m, act ? __ldg(mc + i) : 0.f, (uint32_t)(e0 + i), act, K, nx, ny, nz,
+               &cta_thr);
     while (w.qn >= 32) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
   }
   while (w.qn > 0) warp_flush(w, wq, m, K, nx, ny, nz, &cta_thr);
@@ -227,13 +234,15 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_localmax(const float* __r
 }  // namespace
 
 void launch_topk(Ctx* ctx, const float* map_d, int T, const gh_grid& g, int K, int64_t bin0,
-                 int64_t* idx_d, float* val_d) {
+                 int64_t* idx_d, float* val_d, int64_t e0, int64_t e1) {
   if (K < 1 || K > kMaxK) fail(GH_EINVAL, "top-k: k must be in [1, 8]");
   const int64_t G = (int64_t)g.n[0] * g.n[1] * g.n[2];
   if (G >= 0xffffffffll) fail(GH_EINVAL, "top-k: map above 2^32 - 1 bins");
+  if (e1 < 0) e1 = G;
+  if (e0 < 0 || e0 >= e1 || e1 > G) fail(GH_EINVAL, "top-k: core range outside the map");
   KTimer kt(ctx, "topk");
   k_topk_localmax<<<T, kTopkThreads, 0, ctx->stream>>>(map_d, G, g.n[0], g.n[1], g.n[2], K, bin0,
-                                                       idx_d, val_d);
+                                                       e0, e1, idx_d, val_d);
   GH_LAUNCHED(ctx);
 }
 

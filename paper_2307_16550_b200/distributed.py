@@ -115,3 +115,39 @@ def max_over_ranks(x: float, device=None) -> float:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def merge_topk(bins: np.ndarray, values: np.ndarray, k: int):
+    """Per-trial top-k over candidate lists from several shards: bins/values
+    [S, T, k] (bin -1 = none) -> ([T, k], [T, k]) ranked by (value desc, bin
+    asc), the order of the key above. Exact when every shard reports the k
+    best local maxima of its core layers (halo shards) — a global top-k
+    maximum is a core maximum of exactly one shard and ranks in its top-k."""
+    bins = np.asarray(bins, dtype=np.int64)
+    values = np.asarray(values, dtype=np.float32)
+    S, T, kk = bins.shape
+    keys = encode_keys(np.where(bins >= 0, values, 0.0), np.where(bins >= 0, bins, 0))
+    keys = np.where(bins >= 0, keys, -1).transpose(1, 0, 2).reshape(T, S * kk)
+    order = np.argsort(-keys, axis=1, kind="stable")[:, :k]
+    top = np.take_along_axis(keys, order, axis=1)
+    b, v = decode_keys(np.where(top >= 0, top, 0))
+    return np.where(top >= 0, b, -1), np.where(top >= 0, v, 0.0).astype(np.float32)
+
+
+def allgather_topk(bins: np.ndarray, values: np.ndarray, k: int, device=None):
+    """The c5 multi-target exchange: one all-gather of every
+    rank's k candidates per trial, then merge_topk on each rank."""
+    import torch
+    import torch.distributed as dist
+    bins = np.asarray(bins, dtype=np.int64)
+    values = np.asarray(values, dtype=np.float32)
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        return merge_topk(bins[None], values[None], k)
+    keys = encode_keys(np.where(bins >= 0, values, 0.0), np.where(bins >= 0, bins, 0))
+    keys = np.where(bins >= 0, keys, -1)
+    t = torch.from_numpy(keys).to(device)
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    allk = np.stack([p.cpu().numpy() for p in parts])  # [S, T, k]
+    b, v = decode_keys(np.where(allk >= 0, allk, 0))
+    return merge_topk(np.where(allk >= 0, b, -1), v, k)

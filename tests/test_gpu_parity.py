@@ -471,3 +471,39 @@ def test_full_ring_exact_ties_smallest_bin(ctx, name):
     for k in range(T):
         top = np.flatnonzero(m[k] == m[k].max())
         assert idx[k] == top[0], (k, idx[k], top[:4])
+
+
+@pytest.mark.parametrize("cfg", ["c5", "c3"])
+def test_halo_shards_topk_merge_equals_full_grid(ctx, cfg):
+    # location-grid shards with K targets: each halo shard
+    # reports the top-K maxima of its core layers; merging the shards' K
+    # candidates gives the full grid's top-K exactly
+    from paper_2307_16550_b200 import distributed as D
+    if cfg == "c5":
+        sc, K, T = c5_reduced(), 3, 12
+    else:
+        c3 = S.baseline("c3")
+        sp = c3.grid_spacing[0]
+        nx, ny = 90, 77
+        ox, oy = -sp * (nx - 1) / 2, -sp * (ny - 1) / 2
+        sc = c3.with_(grid_n=(nx, ny, 1), grid_origin=(ox, oy, 0.0), wrap=True,
+                      area_lo=(ox - sp / 2, oy - sp / 2, 0.0), area_hi=(-ox + sp / 2, -oy + sp / 2, 0.0))
+        K, T = 5, 12
+    fr, _ = O.synth(sc, 5, T)
+    fd = frames_to_dev(fr)
+    full = gh.precompute_hop_table(ctx, sc)
+    fi, fv = gh.hop_topk(ctx, full, fd, K)
+    n = sc.slab_axis_len()
+    cuts = [0, n // 3, (2 * n) // 3, n]
+    bs, vs = [], []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        sh = gh.precompute_hop_table_shard(ctx, sc, lo, hi, halo=True)
+        si, sv = gh.hop_topk(ctx, sh, fd, K)
+        b0, b1 = sc.slab_bins(lo, hi)
+        si_ = si.cpu().numpy()
+        assert ((si_ < 0) | ((si_ >= b0) & (si_ < b1))).all()  # core peaks only
+        bs.append(si_)
+        vs.append(sv.cpu().numpy())
+    mb, mv = D.merge_topk(np.stack(bs), np.stack(vs), K)
+    assert np.array_equal(mb, fi.cpu().numpy())
+    assert np.array_equal(mv, fv.cpu().numpy())
