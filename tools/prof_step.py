@@ -24,13 +24,13 @@ def main():
     sc = S.baseline(a.config)
     T = a.trials or sc.trials
     ctx = gh.Context(0)
-    ctx.set_topk_impl("fused" if a.path == "topk" else "auto")
+    ctx.set_topk_impl("fused" if a.path == "topk" else "map" if a.path == "map" else "auto")
     table = gh.precompute_hop_table(ctx, sc) if a.path != "direct" else None
     frames, _ = gh.synthesize(ctx, sc, 0, T)
     for _ in range(a.steps):
         if a.path == "frames":
             gh.hop_argmax(ctx, table, frames)
-        elif a.path == "topk":
+        elif a.path in ("topk", "map"):  # fused engine / map-then-pick engine
             gh.hop_topk(ctx, table, frames, sc.topk)
         elif a.path == "campaign":
             gh.campaign_hop(ctx, table, sc, 0, T)
