@@ -108,10 +108,13 @@ int gh_ctx_reset_timing(gh_ctx* ctx);
  * checked and timed against); 2 = single-stage tcgen05 3xTF32 kernel (v1);
  * 3 = the warp-specialised pipeline in 3xTF32 (kind::tf32). */
 int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
-/* Top-K local-maximum engine (BASELINE c3): 0 = auto (the measured faster
- * one: map then pick), 1 = fused gather + pick (maps stay in shared memory), 2 =
- * map-mode gather then k_topk_localmax over the maps in HBM. Both return
- * identical bins and values. */
+/* Top-K local-maximum engine (BASELINE c3): 0 = auto (engine 3 where the
+ * table's plan admits it — tiled K = 1 plans of at most 16 pairs — and the
+ * call has at least one 8-trial batch per SM, else engine 2); 1 = halo tiles
+ * with the tile's values in shared memory; 2 = map-mode gather, then
+ * k_topk_localmax over the maps in HBM; 3 = the gather with the prune test in
+ * its loop and candidates verified against the table and spectra (no maps).
+ * All engines return identical bins and values. */
 int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl);
 /* Diagnostics: measured shared-memory (LSU) read bandwidth of the device,
  * GB/s, all SMs — the roofline denominator of the gather kernel. */

@@ -262,9 +262,10 @@ class Context:
         _check(lib().gh_ctx_reset_timing(self.h))
 
     def set_topk_impl(self, impl: str) -> None:
-        """'auto' (default), 'fused' (gather + local-maximum pick in shared
-        memory) or 'map' (map-mode gather, then k_topk_localmax on the maps)."""
-        _check(lib().gh_ctx_set_topk_impl(self.h, {"auto": 0, "fused": 1, "map": 2}[impl]))
+        """'auto' (default), 'pick' (gather with the prune test in its loop,
+        no maps), 'fused' (halo tiles, values in shared memory) or 'map'
+        (map-mode gather, then k_topk_localmax on the maps)."""
+        _check(lib().gh_ctx_set_topk_impl(self.h, {"auto": 0, "fused": 1, "map": 2, "pick": 3}[impl]))
 
     def set_direct_impl(self, impl: str) -> None:
         """'tcgen05' (default: warp-specialised 3xFP16 tensor-core pipeline),

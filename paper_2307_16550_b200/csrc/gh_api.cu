@@ -209,8 +209,40 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
 // gather launches fill the GPU), then k_topk_localmax picks the peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
-  // auto (0) takes the map-then-pick path until the fused kernel measures
-  // faster on c3 (top-K)
+  // Engines (gh_ctx_set_topk_impl): 3 = the gather with the prune test in its
+  // loop (gh_gather_pick.cu), 1 = halo tiles with values in shared memory
+  // (gh_gather_topk.cu), 2 = map then pick. auto (0) takes engine 3 where the
+  // plan admits it and there is a batch per SM to hand out, else 2; every
+  // engine returns the same lists.
+  if (c->topk_impl == 0 || c->topk_impl == 3) {
+    const gh::Plan& ap = gh::build_plan(c, t, false);
+    const bool ok = gh::gather_pick_ok(t, ap, K);
+    if (c->topk_impl == 3 && !ok)
+      fail(GH_EINVAL, "top-k: the pick engine needs a tiled K = 1 plan of at most 16 pairs");
+    if (ok && (c->topk_impl == 3 || (T + ap.tb - 1) / ap.tb >= c->num_sms)) {
+      // trial chunks bound the spectra scratch (~16 GiB of the 180 GB) and
+      // split T evenly, so every launch hands each SM many batches
+      const int tb = ap.tb;
+      const int64_t spec_per_trial = (int64_t)t->P * t->M * ap.esize;
+      const int64_t cap = std::max<int64_t>(tb, ((int64_t(1) << 34) / spec_per_trial) / tb * tb);
+      const int64_t n_chunks = (T + cap - 1) / cap;
+      const int64_t chunk = ((T + n_chunks - 1) / n_chunks + tb - 1) / tb * tb;
+      for (int64_t t0 = 0; t0 < T; t0 += chunk) {
+        const int tc = static_cast<int>(std::min<int64_t>(chunk, T - t0));
+        gh::SynthParams sc{};
+        const gh::SynthParams* spc = nullptr;
+        if (sp) {
+          sc = *sp;
+          sc.trial0 += static_cast<uint64_t>(t0);
+          spc = &sc;
+        }
+        const float2* fr = frames ? frames + t0 * t->P * t->N : nullptr;
+        void* spec = gather_spectra(c, t, fr, spc, tc, combine, false);
+        gh::launch_gather_pick(c, t, spec, tc, K, idx_d + t0 * K, val_d + t0 * K);
+      }
+      return;
+    }
+  }
   gh::Plan* tp = c->topk_impl != 1 ? nullptr : gh::build_plan_topk(c, t);
   if (tp) {
     // fused: the gather keeps each tile's values in shared memory and picks
@@ -647,6 +679,7 @@ int gh_ctx_destroy(gh_ctx* ctx) {
     c->amax.release();
     c->misc2.release();
     c->flagbuf.release();
+    c->pickctr.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->ev_ready)
@@ -716,8 +749,10 @@ int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     if (!c) fail(GH_EINVAL, "ctx: null argument");
-    if (impl < 0 || impl > 2)
-      fail(GH_EINVAL, "ctx: top-k impl must be 0 (auto), 1 (fused) or 2 (map then pick)");
+    if (impl < 0 || impl > 3)
+      fail(GH_EINVAL,
+           "ctx: top-k impl must be 0 (auto), 1 (fused halo tiles), 2 (map then pick) or 3 "
+           "(gather + in-loop pick)");
     c->topk_impl = impl;
   });
 }

@@ -60,6 +60,42 @@ __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDes
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
 }
 
+// Exact-tie check of a bank-permuted full-ring plan (see its call in
+// k_gather): for each trial of the batch, re-evaluate the entries of the
+// winner's permutation window from the staged ring and keep the smallest bin
+// among those whose value equals the winner's. Out of line so the gather
+// loop's register allocation is untouched.
+template <int TB, int L, bool CP, int NT>
+__device__ __noinline__ void tie_check(const GatherArgs& a, int P, int64_t entry0, int64_t nb,
+                                       const float* smf, const float* fin_v, const int* fin_i,
+                                       unsigned* fin_b) {
+  for (int job = threadIdx.x; job < TB * kBankWindow; job += NT) {
+    const int tr = job % TB, cnd = job / TB;
+    const int wi = fin_i[tr];
+    if (wi < 0) continue;
+    const int64_t eg = entry0 + wi;
+    const int64_t lb2 = (eg & ~int64_t(kBankWindow - 1)) + cnd - entry0;
+    if (lb2 < 0 || lb2 >= nb || lb2 == wi) continue;
+    float val = 0.f;
+    if constexpr (CP) {
+      const unsigned wd = __ldg(a.crow + entry0 + lb2);
+      const unsigned mask = (1u << a.cbits) - 1u;
+      for (int p = 0; p < P; ++p) {
+        const unsigned r = (wd >> (a.cbits * p)) & mask;
+        const float z = smf[(size_t)((unsigned)(p * a.ring + r) * L) * 4 + tr];
+        val = p == 0 ? z : __fadd_rn(val, z);
+      }
+    } else {
+      for (int p = 0; p < P; ++p) {
+        const unsigned o = a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb2) * 4 + (p & 3)];
+        const float z = smf[(size_t)o * 4 + tr];
+        val = p == 0 ? z : __fadd_rn(val, z);
+      }
+    }
+    if (val == fin_v[tr]) atomicMin(&fin_b[tr], __ldg(a.binid + entry0 + lb2));
+  }
+}
+
 // PC: compile-time pair count (0 = runtime, at most 4 * PQ)
 // CP (compact rows, full-ring K = 1 plans with P * bits(ring) <= 32): one
 // 32-bit word per bin holds every pair's ring row, so a step needs a single
@@ -75,6 +111,9 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ float red_v[NW * TB];
   __shared__ int red_i[NW * TB];
+  __shared__ float fin_v[TB];
+  __shared__ int fin_i[TB];
+  __shared__ unsigned fin_b[TB];
 
   const int P = PC ? PC : a.P;
   __shared__ __align__(8) uint64_t stage_bar;
@@ -247,13 +286,6 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
             if (vals[i] > best[i]) {
               best[i] = vals[i];
               blb[i] = (int)lb;
-            } else if (FULL && vals[i] == best[i] && a.binid &&
-                       __ldg(a.binid + entry0 + lb) < __ldg(a.binid + entry0 + blb[i])) {
-              // bank-permuted entries are not in bin order: an exact tie
-              // (zero frames, mirror-symmetric layouts) keeps the smaller
-              // bin, argmax_index's rule (src/direct.cpp:55-62); rare, so
-              // the two id loads stay off the common path
-              blb[i] = (int)lb;
             }
           }
         }
@@ -310,10 +342,47 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
         }
       }
       const int trial = tb * TB + threadIdx.x;
-      if (trial < a.T && bi >= 0) {
-        const unsigned long long gb = (unsigned long long)global_bin(a, td, entry0, bi);
-        atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
-                                      (0xffffffffull - gb));
+      unsigned long long gb = bi >= 0 ? (unsigned long long)global_bin(a, td, entry0, bi) : 0ull;
+      if constexpr (FULL && !K3) {
+        if (a.binid) {
+          fin_v[threadIdx.x] = bv;
+          fin_i[threadIdx.x] = bi;
+          fin_b[threadIdx.x] = bi >= 0 ? (unsigned)gb : 0xffffffffu;
+        }
+      }
+      if constexpr (!(FULL && !K3)) {
+        if (trial < a.T && bi >= 0)
+          atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                        (0xffffffffull - gb));
+      } else if (!a.binid) {
+        if (trial < a.T && bi >= 0)
+          atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
+                                        (0xffffffffull - gb));
+      }
+    }
+    if constexpr (FULL && !K3) {
+      if (a.binid) {
+        // Bank-permuted entries are in bin order only across the
+        // kBankWindow-entry windows of permute_for_banks, and a lane keeps
+        // the first strict maximum of its entries. An exact tie inside the
+        // winner's window (zero frames, noiseless mirror-symmetric scenes)
+        // could therefore keep a larger bin than argmax_index's first maximum
+        // (src/direct.cpp:55-62). The ring is still staged: re-evaluate that
+        // window's entries (same pair order, same adds) and let an equal
+        // value with a smaller bin take over. ~6 entries per thread and
+        // item, out of line (tie_check), nothing in the gather loop.
+        __syncthreads();
+        tie_check<TB, L, CP, kGatherThreads>(a, P, entry0, nb,
+                                             reinterpret_cast<const float*>(smraw), fin_v, fin_i,
+                                             fin_b);
+        __syncthreads();
+        if (threadIdx.x < TB) {
+          const int trial = tb * TB + threadIdx.x;
+          if (trial < a.T && fin_i[threadIdx.x] >= 0)
+            atomicMax(a.keys + trial,
+                      ((unsigned long long)__float_as_uint(fin_v[threadIdx.x]) << 32) |
+                          (0xffffffffull - (unsigned long long)fin_b[threadIdx.x]));
+        }
       }
     }
   }

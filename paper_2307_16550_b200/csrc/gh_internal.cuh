@@ -61,9 +61,10 @@ struct Ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t smem_optin = 227 * 1024;
-  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2, flagbuf;
+  Buffer spectra, frames, keys, misc, twiddle_buf, aprep, mapbuf, seeds, amax, misc2, flagbuf,
+      pickctr;
   int twiddle_m = 0;
-  int topk_impl = 0;    // 0: auto, 1: fused gather + pick, 2: map then pick
+  int topk_impl = 0;    // 0: auto, 1: fused halo tiles, 2: map then pick, 3: gather + in-loop pick
   int direct_impl = 0;  // 0: tcgen05 3xFP16, 1: CUDA-core fp32, 2: tcgen05 v1, 3: tcgen05 3xTF32
   // host-buffer entry points: copy stream, double-buffer events, pinned staging
   cudaStream_t copy_stream = nullptr;
@@ -171,6 +172,11 @@ __host__ __device__ __forceinline__ void tile_local(const TileDesc& td, int64_t 
     *lz = lb / ((int64_t)td.wx * td.wy);
   }
 }
+
+// entries per bank-permutation window of a full-ring plan (permute_for_banks
+// orders bins freely inside a window, windows stay in bin order; k_gather's
+// exact-tie check re-evaluates one window)
+constexpr int kBankWindow = 256;
 
 struct Plan {
   bool built = false;
@@ -290,6 +296,12 @@ Plan* build_plan_topk(Ctx* ctx, Table* t);
 // cand_d [T][n_tiles][K] (thr_d [T] zeroed by the caller), then the merge
 void launch_gather_topk(Ctx* ctx, Table* t, const void* spec_d, int T, int K,
                         unsigned long long* cand_d, unsigned long long* thr_d);
+// gather + top-K pick with the prune test in the gather loop (gh_gather_pick.cu):
+// the argmax plan's tiles, one CTA per 8-trial batch, results straight to
+// idx_d / val_d [T][K]
+bool gather_pick_ok(const Table* t, const Plan& pl, int K);
+void launch_gather_pick(Ctx* ctx, Table* t, const void* spec_d, int T, int K, int64_t* idx_d,
+                        float* val_d);
 void launch_topk_merge(Ctx* ctx, const unsigned long long* cand_d, int T, int n_lists, int K,
                        int64_t* idx_d, float* val_d);
 void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine,

@@ -409,7 +409,7 @@ constexpr size_t kTileBudget = 216 * 1024;   // tiled plans: one CTA per SM
 // when their row indices have equal parity. Bins are re-ordered so that
 // entries (2k, 2k+1) have complementary parity vectors over the pairs
 // wherever possible (greedy matching of vector v with ~v within windows of
-// 1024 bins); `binid` maps entries back to bins, which keeps reported
+// kBankWindow bins); `binid` maps entries back to bins, which keeps reported
 // indices and the smallest-bin tie rule exact.
 void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   const int P = t->P, p4 = pl.p4, L = pl.tb * pl.esize / 16;
@@ -448,7 +448,7 @@ void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   }
   std::vector<uint32_t> order;
   order.reserve(static_cast<size_t>(n));
-  constexpr int64_t W = 1024;  // even: pairs stay on even entry offsets
+  constexpr int64_t W = kBankWindow;  // even: pairs stay on even entry offsets
   std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
   const int64_t nu = static_cast<int64_t>(uniq.size());
   for (int64_t w0 = 0; w0 < nu; w0 += W) {

@@ -1,4 +1,6 @@
-"""Fused gather + top-K local maxima (gh_gather.cu k_gather_topk) against the
+"""Map-free top-K local maxima — the gather with the prune test in its loop
+(gh_gather_pick.cu k_gather_pick, engine "pick") and the halo-tile kernel
+(gh_gather_topk.cu k_gather_topk, engine "fused") — against the
 map-then-pick path (k_gather map mode + k_topk_localmax, the same fp32
 values) and the fp64 oracle.
 
@@ -22,11 +24,11 @@ from test_gpu_parity import frames_to_dev, topk_parity
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def fused_engine(ctx):
-    # these tests pin the fused engine; the session context is shared
-    ctx.set_topk_impl("fused")
-    yield
+@pytest.fixture(autouse=True, params=["pick", "fused"])
+def fused_engine(ctx, request):
+    # these tests pin the map-free engine; the session context is shared
+    ctx.set_topk_impl(request.param)
+    yield request.param
     ctx.set_topk_impl("auto")
 
 
@@ -114,3 +116,47 @@ def test_topk_engines_agree_on_a_ragged_batch(ctx):
     mi, mv = gh.hop_topk(ctx, t, fd, k)
     assert np.array_equal(fi.cpu().numpy(), mi.cpu().numpy())
     assert np.array_equal(fv.cpu().numpy(), mv.cpu().numpy())
+
+
+def test_pick_3d_grid_and_halo_shards(ctx, fused_engine):
+    # the pick engine on a 3-D lattice (26 neighbours) and on halo shards
+    # (core layers only, neighbours inside the shard's layers): identical to
+    # the map engine through the same entry point
+    if fused_engine != "pick":
+        pytest.skip("the halo-tile kernel is 2-D only")
+    from test_gpu_parity import c5_reduced
+    c5 = c5_reduced()
+    sc = c5.with_(tx=c5.tx[:12], rx=c5.rx[:12])  # 12 pairs: a tiled plan the engine takes
+    T, k = 21, 3
+    fr, _ = O.synth(sc, 9, T)
+    fd = frames_to_dev(fr)
+    tables = [gh.precompute_hop_table(ctx, sc),
+              gh.precompute_hop_table_shard(ctx, sc, 2, 5, halo=True),
+              gh.precompute_hop_table_shard(ctx, sc, 0, 3, halo=False)]
+    for t in tables:
+        ctx.set_topk_impl("pick")
+        pi, pv = gh.hop_topk(ctx, t, fd, k)
+        ctx.set_topk_impl("map")
+        mi, mv = gh.hop_topk(ctx, t, fd, k)
+        assert np.array_equal(pi.cpu().numpy(), mi.cpu().numpy())
+        assert np.array_equal(pv.cpu().numpy(), mv.cpu().numpy())
+    oi, oc, _ = O.build_table(sc)
+    ref = O.hop_map(O.spectra(fr, sc.n_fft), oi, oc)
+    ctx.set_topk_impl("pick")
+    pi, _ = gh.hop_topk(ctx, tables[0], fd, k)
+    topk_parity(ref, pi.cpu().numpy(), sc, k, "pick 3-D")
+
+
+def test_auto_engine_takes_pick_on_large_batches(ctx, fused_engine):
+    # auto: >= one 8-trial batch per SM -> the pick engine; same lists as map
+    if fused_engine != "pick":
+        pytest.skip("engine-independent")
+    sc = c3_sub(96, 82)
+    T, k = 8 * 148 + 5, 5
+    t = gh.precompute_hop_table(ctx, sc)
+    ctx.set_topk_impl("auto")
+    ai, av = gh.campaign_hop_topk(ctx, t, sc, 0, T, k)
+    ctx.set_topk_impl("map")
+    mi, mv = gh.campaign_hop_topk(ctx, t, sc, 0, T, k)
+    assert np.array_equal(ai.cpu().numpy(), mi.cpu().numpy())
+    assert np.array_equal(av.cpu().numpy(), mv.cpu().numpy())

@@ -1,5 +1,5 @@
-"""Time the c3 top-K paths on one trial chunk: fused gather+pick
-(gh_hop_topk_d) vs map-then-pick (hop_decision_map + topk_local_max).
+"""Time the c3 top-K engines on one trial chunk: pick (prune test in the
+gather loop), fused (halo tiles) and map-then-pick, all through gh_hop_topk_d.
 
     python tools/time_topk.py [--trials 2048] [--steps 3]
 """
@@ -20,17 +20,19 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--trials", type=int, default=2048)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--engines", default="pick,fused,map")
+    ap.add_argument("--k", type=int, default=0, help="top-k (0: the scene's)")
+    ap.add_argument("--warm", type=int, default=2)
     a = ap.parse_args()
     sc = S.baseline(a.config)
     ctx = gh.Context(0)
-    ctx.set_topk_impl("fused")
     table = gh.precompute_hop_table(ctx, sc)
     fr, _ = gh.synthesize(ctx, sc, 0, a.trials)
     ctx.synchronize()
     stream = ctx.torch_stream()
 
     def timed(name, fn):
-        for _ in range(2):
+        for _ in range(a.warm):
             fn()
         ctx.synchronize()
         ctx.reset_timing()
@@ -48,11 +50,14 @@ def main():
         print(f"{name}: {e0.elapsed_time(e1) / a.steps:.3f} ms/step  kernels {ks}", flush=True)
         return out
 
-    fi, fv = timed("fused", lambda: gh.hop_topk(ctx, table, fr, sc.topk))
-    ctx.set_topk_impl("map")
-    ui, uv = timed("map+pick", lambda: gh.topk_local_max(ctx, sc, gh.hop_decision_map(ctx, table, fr),
-                                                        sc.topk))
-    print("same idx:", bool(torch.equal(fi, ui)), "same val:", bool(torch.equal(fv, uv)))
+    outs = {}
+    for eng in a.engines.split(","):
+        ctx.set_topk_impl(eng)
+        outs[eng] = timed(eng, lambda: gh.hop_topk(ctx, table, fr, a.k or sc.topk))
+    base = a.engines.split(",")[-1]
+    for eng, (i, v) in outs.items():
+        print(eng, "vs", base, "same idx:", bool(torch.equal(i, outs[base][0])), "same val:",
+              bool(torch.equal(v, outs[base][1])))
 
 
 if __name__ == "__main__":
