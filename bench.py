@@ -56,9 +56,10 @@ def peaks() -> dict:
 # gather instantiation per BASELINE config: its ncu --set full capture in
 # profiles/ supplies roofline.traffic (DRAM read + write per launch)
 GATHER_KERNEL = {"c1": "k_gather<16, 0, 0, 0, 3, 1", "c2": "k_gather<16, 0, 0, 0, 3, 1",
-                 "c3": "k_gather<8, 0, 0, 1, 16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
+                 "c3": "k_gather_pick<16, 4>", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
 GATHER_LABEL = {"c1": "k_gather (fused argmax)", "c2": "k_gather (fused argmax)",
-                "c3": "k_gather (map mode) + k_topk_localmax", "c4": "k_gather (K = 3, fused argmax)"}
+                "c3": "k_gather_pick (gather with the top-K prune test in its loop, no maps)",
+                "c4": "k_gather (K = 3, fused argmax)"}
 
 
 def ncu_traffic(config: str, trials: int):
@@ -74,16 +75,17 @@ def ncu_traffic(config: str, trials: int):
     for rep, kernels in data.items():
         for k in kernels:
             if want in k.get("kernel", "") and k.get("dram_read_bytes") is not None:
-                t0 = PROFILE_TRIALS.get(rep)
+                t0 = next((n for pre, n in PROFILE_TRIALS.items() if rep.startswith(pre + "_r")),
+                          None)
                 if not t0:
                     continue
                 return (k["dram_read_bytes"] + k.get("dram_write_bytes", 0.0)) * trials / t0
     return None
 
 
-# trials per launch of each committed capture (tools/evidence.sh)
-PROFILE_TRIALS = {"prof_hop_r1.ncu-rep": 10000, "prof_c3_r1.ncu-rep": 2048,
-                  "prof_direct_r1.ncu-rep": 1024}
+# trials per launch of each committed capture (tools/evidence*.sh), by report prefix
+PROFILE_TRIALS = {"prof_hop": 10000, "prof_c3": 2048, "prof_c3fused": 2048, "prof_c3pick": 9472,
+                  "prof_c4": 2000, "prof_c5": 64, "prof_direct": 1024}
 
 
 class ClockSampler:

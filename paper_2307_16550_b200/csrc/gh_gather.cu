@@ -60,39 +60,41 @@ __device__ __forceinline__ int64_t global_bin(const GatherArgs& a, const TileDes
   return (td.x0 + lx) + (int64_t)a.grid.n[0] * ((td.y0 + ly) + (int64_t)a.grid.n[1] * (td.z0 + lz));
 }
 
-// Exact-tie check of a bank-permuted full-ring plan (see its call in
-// k_gather): for each trial of the batch, re-evaluate the entries of the
-// winner's permutation window from the staged ring and keep the smallest bin
-// among those whose value equals the winner's. Out of line so the gather
-// loop's register allocation is untouched.
+// Exact ties on a bank-permuted full-ring plan. Its ordered part gives every
+// lane its bins in increasing order, so the first strict maximum is the
+// smallest bin; only a tail entry (a.tie_from on) can tie with a lane's
+// running maximum from a larger bin. The gather flags that; here, for the
+// flagged trials, the tail entries of the item are re-evaluated from the
+// staged ring (same pair order, same adds) and the smallest bin among those
+// equal to the item's maximum takes over — argmax_index's first maximum
+// (src/direct.cpp:55-62). Out of line: zero frames and noiseless
+// mirror-symmetric scenes get here, nothing else.
 template <int TB, int L, bool CP, int NT>
-__device__ __noinline__ void tie_check(const GatherArgs& a, int P, int64_t entry0, int64_t nb,
-                                       const float* smf, const float* fin_v, const int* fin_i,
+__device__ __noinline__ void tail_scan(const GatherArgs& a, int P, int64_t entry0, int64_t nb,
+                                       const float* smf, unsigned mask, const float* fin_v,
                                        unsigned* fin_b) {
-  for (int job = threadIdx.x; job < TB * kBankWindow; job += NT) {
-    const int tr = job % TB, cnd = job / TB;
-    const int wi = fin_i[tr];
-    if (wi < 0) continue;
-    const int64_t eg = entry0 + wi;
-    const int64_t lb2 = (eg & ~int64_t(kBankWindow - 1)) + cnd - entry0;
-    if (lb2 < 0 || lb2 >= nb || lb2 == wi) continue;
+  const int64_t lo = a.tie_from > entry0 ? a.tie_from - entry0 : 0;
+  for (int64_t job = threadIdx.x; job < (nb - lo) * TB; job += NT) {
+    const int tr = (int)(job % TB);
+    if (!((mask >> tr) & 1u)) continue;
+    const int64_t lb = lo + job / TB;
     float val = 0.f;
     if constexpr (CP) {
-      const unsigned wd = __ldg(a.crow + entry0 + lb2);
-      const unsigned mask = (1u << a.cbits) - 1u;
+      const unsigned wd = __ldg(a.crow + entry0 + lb);
+      const unsigned m = (1u << a.cbits) - 1u;
       for (int p = 0; p < P; ++p) {
-        const unsigned r = (wd >> (a.cbits * p)) & mask;
+        const unsigned r = (wd >> (a.cbits * p)) & m;
         const float z = smf[(size_t)((unsigned)(p * a.ring + r) * L) * 4 + tr];
         val = p == 0 ? z : __fadd_rn(val, z);
       }
     } else {
       for (int p = 0; p < P; ++p) {
-        const unsigned o = a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb2) * 4 + (p & 3)];
+        const unsigned o = a.rows[((int64_t)(p >> 2) * a.n_entries + entry0 + lb) * 4 + (p & 3)];
         const float z = smf[(size_t)o * 4 + tr];
         val = p == 0 ? z : __fadd_rn(val, z);
       }
     }
-    if (val == fin_v[tr]) atomicMin(&fin_b[tr], __ldg(a.binid + entry0 + lb2));
+    if (val == fin_v[tr]) atomicMin(&fin_b[tr], __ldg(a.binid + entry0 + lb));
   }
 }
 
@@ -111,9 +113,9 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ float red_v[NW * TB];
   __shared__ int red_i[NW * TB];
-  __shared__ float fin_v[TB];
-  __shared__ int fin_i[TB];
-  __shared__ unsigned fin_b[TB];
+  __shared__ float fin_v[TB];     // full-ring plans: the item's winners, settled by tail_scan
+  __shared__ unsigned fin_b[TB];  // ... their bins
+  __shared__ unsigned tie_mask;   // trials whose running maximum tied with a tail entry
 
   const int P = PC ? PC : a.P;
   __shared__ __align__(8) uint64_t stage_bar;
@@ -167,6 +169,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   uint4* sm4 = reinterpret_cast<uint4*>(smraw);
   __syncthreads();  // barrier initialised / previous item's readers done
   if (threadIdx.x == 0) {
+    tie_mask = 0u;  // before the staging it arms: no warp gathers earlier
     uint32_t total = 0;
     for (int p = 0; p < P; ++p) total += (uint32_t)win[p].y * 16u * L;
     mbar_expect_tx(&stage_bar, total);
@@ -232,7 +235,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
     // one step: lane group `sub` handles bin j = s * BPW + sub of the block
-    auto step = [&](int s, bool check) {
+    auto step = [&](int s, bool check, bool tie) {
       const int j = s * BPW + sub;
       const int64_t lb = blk + (!check || j < nblk ? j : 0);
       float2 acc[2];
@@ -286,22 +289,36 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
             if (vals[i] > best[i]) {
               best[i] = vals[i];
               blb[i] = (int)lb;
+            } else if (FULL && tie && vals[i] == best[i]) {
+              // an entry of the plan's unordered tail ties with the lane's
+              // running maximum: flag the trial, the item's epilogue settles
+              // it (tail_scan); rare, and only tail blocks test for it
+              atomicOr(&tie_mask, 1u << (v * TPL + i));
             }
           }
         }
       }
     };
     constexpr bool kUnroll = !K3 && PC > 0 && PC <= 16;
+    // bank-permuted full plans: a lane meets the bins of the ordered part in
+    // increasing order (first strict maximum = smallest bin); blocks reaching
+    // into the unordered tail also flag exact ties
+    const bool tie = FULL && a.binid && entry0 + blk + 32 > a.tie_from;
     if (nblk == 32 && kUnroll) {
       // full block: fixed trip count, no bounds checks, fully unrolled so
       // the next step's shuffles and loads overlap this step's updates
+      if (!tie) {
 #pragma unroll
-      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
+        for (int s = 0; s < 32 / BPW; ++s) step(s, false, false);
+      } else {
+#pragma unroll
+        for (int s = 0; s < 32 / BPW; ++s) step(s, false, true);
+      }
     } else if (nblk == 32) {
 #pragma unroll 1
-      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
+      for (int s = 0; s < 32 / BPW; ++s) step(s, false, tie);
     } else {
-      for (int s = 0; s * BPW < nblk; ++s) step(s, true);
+      for (int s = 0; s * BPW < nblk; ++s) step(s, true, tie);
     }
 #pragma unroll
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
@@ -342,47 +359,30 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
         }
       }
       const int trial = tb * TB + threadIdx.x;
-      unsigned long long gb = bi >= 0 ? (unsigned long long)global_bin(a, td, entry0, bi) : 0ull;
+      const unsigned long long gb =
+          bi >= 0 ? (unsigned long long)global_bin(a, td, entry0, bi) : 0ull;
       if constexpr (FULL && !K3) {
-        if (a.binid) {
-          fin_v[threadIdx.x] = bv;
-          fin_i[threadIdx.x] = bi;
-          fin_b[threadIdx.x] = bi >= 0 ? (unsigned)gb : 0xffffffffu;
-        }
-      }
-      if constexpr (!(FULL && !K3)) {
-        if (trial < a.T && bi >= 0)
-          atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
-                                        (0xffffffffull - gb));
-      } else if (!a.binid) {
+        fin_v[threadIdx.x] = bv;
+        fin_b[threadIdx.x] = bi >= 0 ? (unsigned)gb : 0xffffffffu;
+      } else {
         if (trial < a.T && bi >= 0)
           atomicMax(a.keys + trial, ((unsigned long long)__float_as_uint(bv) << 32) |
                                         (0xffffffffull - gb));
       }
     }
     if constexpr (FULL && !K3) {
-      if (a.binid) {
-        // Bank-permuted entries are in bin order only across the
-        // kBankWindow-entry windows of permute_for_banks, and a lane keeps
-        // the first strict maximum of its entries. An exact tie inside the
-        // winner's window (zero frames, noiseless mirror-symmetric scenes)
-        // could therefore keep a larger bin than argmax_index's first maximum
-        // (src/direct.cpp:55-62). The ring is still staged: re-evaluate that
-        // window's entries (same pair order, same adds) and let an equal
-        // value with a smaller bin take over. ~6 entries per thread and
-        // item, out of line (tie_check), nothing in the gather loop.
+      __syncthreads();
+      if (tie_mask) {  // CTA-uniform; only degenerate inputs get here
+        tail_scan<TB, L, CP, kGatherThreads>(a, P, entry0, nb, reinterpret_cast<const float*>(smraw),
+                                             tie_mask, fin_v, fin_b);
         __syncthreads();
-        tie_check<TB, L, CP, kGatherThreads>(a, P, entry0, nb,
-                                             reinterpret_cast<const float*>(smraw), fin_v, fin_i,
-                                             fin_b);
-        __syncthreads();
-        if (threadIdx.x < TB) {
-          const int trial = tb * TB + threadIdx.x;
-          if (trial < a.T && fin_i[threadIdx.x] >= 0)
-            atomicMax(a.keys + trial,
-                      ((unsigned long long)__float_as_uint(fin_v[threadIdx.x]) << 32) |
-                          (0xffffffffull - (unsigned long long)fin_b[threadIdx.x]));
-        }
+      }
+      if (threadIdx.x < TB) {
+        const int trial = tb * TB + threadIdx.x;
+        if (trial < a.T && fin_b[threadIdx.x] != 0xffffffffu)
+          atomicMax(a.keys + trial,
+                    ((unsigned long long)__float_as_uint(fin_v[threadIdx.x]) << 32) |
+                        (0xffffffffull - (unsigned long long)fin_b[threadIdx.x]));
       }
     }
   }
@@ -735,6 +735,7 @@ void launch_gather(Ctx* ctx, Table* t, const void* spec_d, int T, int combine, f
   a.coefr = pl.coefr_d;
   a.binid = pl.full ? pl.binid_d : nullptr;
   a.crow = pl.full ? pl.crow_d : nullptr;
+  a.tie_from = pl.tie_from;
   a.cbits = pl.cbits;
   a.ring = t->M;
   a.grid = t->grid;

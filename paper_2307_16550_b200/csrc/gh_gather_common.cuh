@@ -19,6 +19,7 @@ struct GatherArgs {
   const float2* coef3;    // [P][3][entries] (word-major), complex weights (poly3, linear)
   const float4* coefr;    // [P][entries] real weights (w0, w1, w2, 0): polar tables, else null
   const uint32_t* binid;  // [entries] global bin (bank-permuted full plan), or null
+  int64_t tie_from;       // permuted plan: entries from here on are not in per-lane bin order
   const uint32_t* crow;   // [entries] compact rows: P ring rows of cbits each, or null
   int cbits;              // bits per ring row in crow
   int ring;               // staged rows per pair (full-ring plan)

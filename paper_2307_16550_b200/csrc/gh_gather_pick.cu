@@ -76,6 +76,21 @@ __device__ __forceinline__ float unord_f(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
+// plan row words: read once per batch by every CTA, so they should stay in
+// L2 while the batches' spectra stream through it (evict-last policy)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint2 ldg_keep(const uint2* p, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 // insert key ck into the warp's sorted register list (lane k < K: k-th key)
 __device__ __forceinline__ void list_insert(unsigned long long& mine, unsigned long long ck, int K,
                                             int lane) {
@@ -210,6 +225,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);                  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint4* sm4 = reinterpret_cast<uint4*>(smraw);
+  const uint64_t keep = l2_keep_policy();
   // this warp's candidate queue (global memory, L2-resident; rarely written)
   uint2* queue = pk.queue + ((size_t)blockIdx.x * NW + warp) * kPickQueue;
 
@@ -243,12 +259,17 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
       const int nb = tdp->wx * tdp->wy * tdp->wz;
       const int4* win = a.win + (int64_t)tile * a.P;
       __syncthreads();  // the previous tile's readers are done (and sh.thr / sh.spec are set)
-      if (threadIdx.x == 0) {
+      if (warp == 0) {
+        // the tile's windows by TMA bulk copies, one pair per lane (the
+        // window descriptors load in parallel); then the next tile's windows
+        // are asked into L2 so its staging does not wait on HBM
         uint32_t total = 0;
-        for (int p = 0; p < P; ++p) total += (uint32_t)win[p].y * 16u * L;
-        mbar_expect_tx(&stage_bar, total);
-        for (int p = 0; p < P; ++p) {
-          const int4 w = win[p];
+        for (int p = lane; p < P; p += 32) total += (uint32_t)__ldg(&win[p].y) * 16u * L;
+        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFullMask, total, o);
+        if (lane == 0) mbar_expect_tx(&stage_bar, total);
+        __syncwarp();
+        for (int p = lane; p < P; p += 32) {
+          const int4 w = __ldg(&win[p]);
           const uint4* src = spec + (int64_t)p * a.M * L;
           uint4* dst = sm4 + (int64_t)w.z * L;
           for (int r = 0, gi = w.x; r < w.y; gi = 0) {  // base in [0, M): split where it wraps
@@ -258,14 +279,25 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
             r += n;
           }
         }
-        mbar_arrive(&stage_bar);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stage_bar);
+        if (ti + 1 < a.n_tiles) {
+          const int4* nwin = a.win + (int64_t)(ti + 1) * a.P;
+          for (int p = lane; p < P; p += 32) {
+            const int4 w = __ldg(&nwin[p]);
+            const uint4* src = spec + (int64_t)p * a.M * L;
+            for (int r = 0, gi = w.x; r < w.y; gi = 0) {
+              const int n = a.M - gi < w.y - r ? a.M - gi : w.y - r;
+              bulk_prefetch_l2(src + (int64_t)gi * L, (uint32_t)n * 16u * L);
+              r += n;
+            }
+          }
+        }
       }
       const int per_warp = ((nb + NW - 1) / NW + BPW - 1) / BPW * BPW;
       const int w0 = warp * per_warp < nb ? warp * per_warp : nb;
       const int w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
       const bool blk24 = tdp->blk == 1 + 1 + (2 << 2);  // 2 x 4 x 1 entry blocks
-      mbar_wait(&stage_bar, phase);
-      phase ^= 1u;
       // One run over the warp's entries from block `from` until its end or
       // until the queue could overflow in the next block; returns where to
       // resume. The queue is drained between runs, outside the loop, so no
@@ -279,17 +311,20 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         if (from + lane < w1) {
 #pragma unroll
           for (int q = 0; q < PQ; ++q)
-            if (q < pq) cur[q] = __ldg(rows2 + q * a.n_entries + entry0 + from + lane);
+            if (q < pq) cur[q] = ldg_keep(rows2 + q * a.n_entries + entry0 + from + lane, keep);
         }
         float sbest[4] = {-1.0f, -1.0f, -1.0f, -1.0f};  // SEED: this lane's largest values
         int sblb[4] = {-1, -1, -1, -1};
+        // the tile's windows (the first row words load meanwhile; a later run
+        // of the same tile finds the phase complete)
+        mbar_wait(&stage_bar, phase);
         int blk = from;
         for (; blk < w1; blk += 32) {
           if (qn > kPickQueue - 256) break;  // a block pushes at most 2 x 32 x 4 entries
           if (blk + 32 + lane < w1) {
 #pragma unroll
             for (int q = 0; q < PQ; ++q)
-              if (q < pq) nxt[q] = __ldg(rows2 + q * a.n_entries + entry0 + blk + 32 + lane);
+              if (q < pq) nxt[q] = ldg_keep(rows2 + q * a.n_entries + entry0 + blk + 32 + lane, keep);
           }
           float thr[4];
           if constexpr (!SEED)  // one volatile LDS.128: other warps raise these values
@@ -402,6 +437,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         if (qn) drain_candidates(queue, qn, tdp, &sh);
         if (from >= w1) break;
       }
+      phase ^= 1u;
     }
     __syncthreads();  // every warp's candidates are in the lists
     const int K = pk.K;

@@ -173,11 +173,6 @@ __host__ __device__ __forceinline__ void tile_local(const TileDesc& td, int64_t 
   }
 }
 
-// entries per bank-permutation window of a full-ring plan (permute_for_banks
-// orders bins freely inside a window, windows stay in bin order; k_gather's
-// exact-tie check re-evaluates one window)
-constexpr int kBankWindow = 256;
-
 struct Plan {
   bool built = false;
   bool full = false;
@@ -194,6 +189,7 @@ struct Plan {
   float2* coef3_d = nullptr;     // [P][3][entries] complex weights (k3, complex schemes)
   float4* coefr_d = nullptr;     // [P][entries] real weights (k3 polar tables), instead of coef3_d
   uint32_t* binid_d = nullptr;   // [entries] global bin of each entry (permuted plans)
+  int64_t tie_from = 0;          // permuted plans: first entry of the unordered tail (see permute_for_banks)
   uint32_t* crow_d = nullptr;    // [entries] compact ring rows (cbits per pair), or null
   int cbits = 0;
   int64_t n_entries = 0;

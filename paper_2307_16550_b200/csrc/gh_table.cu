@@ -407,10 +407,10 @@ constexpr size_t kTileBudget = 216 * 1024;   // tiled plans: one CTA per SM
 // there is 64 bytes (half a shared-memory wavefront) and the gather serves
 // two bins per quarter-warp with one LDS.128 per pair: the two rows collide
 // when their row indices have equal parity. Bins are re-ordered so that
-// entries (2k, 2k+1) have complementary parity vectors over the pairs
-// wherever possible (greedy matching of vector v with ~v within windows of
-// kBankWindow bins); `binid` maps entries back to bins, which keeps reported
-// indices and the smallest-bin tie rule exact.
+// entries (2k, 2k+1) have complementary parity vectors over the pairs;
+// `binid` maps entries back to bins, which keeps reported indices exact, and
+// the order is built so that the smallest-bin tie rule of argmax_index
+// (src/direct.cpp:55-62) survives it (see the two cases below).
 void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   const int P = t->P, p4 = pl.p4, L = pl.tb * pl.esize / 16;
   const int64_t n = pl.n_entries;
@@ -448,34 +448,74 @@ void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   }
   std::vector<uint32_t> order;
   order.reserve(static_cast<size_t>(n));
-  constexpr int64_t W = kBankWindow;  // even: pairs stay on even entry offsets
-  std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
   const int64_t nu = static_cast<int64_t>(uniq.size());
-  for (int64_t w0 = 0; w0 < nu; w0 += W) {
-    const int64_t w1 = std::min<int64_t>(nu, w0 + W);
-    for (auto& b : bucket) b.clear();
-    for (int64_t u = w1 - 1; u >= w0; --u) {  // reversed: pop_back yields ascending
-      const uint32_t e = uniq[static_cast<size_t>(u)];
-      unsigned v = 0;
-      for (int p = 0; p < P; ++p) v |= ((rows[static_cast<size_t>(e) * p4 + p] / L) & 1u) << p;
-      bucket[v].push_back(e);
-    }
-    std::vector<uint32_t> rest;
-    for (unsigned v = 0; v <= full; ++v) {
-      auto& a = bucket[v];
-      auto& b = bucket[full ^ v];
-      if (v > (full ^ v)) continue;  // each complementary couple once
-      while (!a.empty() && !b.empty() && (&a != &b || a.size() >= 2)) {
-        order.push_back(a.back());
-        a.pop_back();
-        order.push_back(b.back());
-        b.pop_back();
+  auto parity = [&](uint32_t e) {
+    unsigned v = 0;
+    for (int p = 0; p < P; ++p) v |= ((rows[static_cast<size_t>(e) * p4 + p] / L) & 1u) << p;
+    return v;
+  };
+  std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
+  if (P <= 3) {
+    // Ordered plan. At most 4 complementary couples (v, ~v) and the gather's
+    // 8 lane groups (entry mod 8) form 4 entry pairs: pair class j takes its
+    // couple's bins in increasing order (entries 8m + 2j, 8m + 2j + 1 = the
+    // couple's next bin of class v and of class ~v). Every entry pair is
+    // bank-complementary, and every lane group meets its bins in increasing
+    // order — so the gather's "first strict maximum" per lane is the
+    // smallest bin on exact ties, with nothing extra in its loop. The bins
+    // left when the shortest couple runs out (class counts differ by a few
+    // per cent) follow in ascending order; from there on (tie_from) the
+    // gather compares bins on exact ties.
+    for (int64_t u = 0; u < nu; ++u) bucket[parity(uniq[static_cast<size_t>(u)])].push_back(uniq[static_cast<size_t>(u)]);
+    const int ncpl = 1 << (P - 1), per = 4 / ncpl;
+    int64_t steps = INT64_MAX;
+    for (int c = 0; c < ncpl; ++c)
+      steps = std::min<int64_t>(
+          steps, static_cast<int64_t>(std::min(bucket[c].size(), bucket[full ^ c].size())) / per);
+    steps -= steps % 4;  // the ordered part ends on a 32-entry block
+    for (int64_t m = 0; m < steps; ++m)
+      for (int j = 0; j < 4; ++j) {
+        const int c = j / per;
+        const size_t i = static_cast<size_t>(m * per + j % per);
+        order.push_back(bucket[c][i]);
+        order.push_back(bucket[full ^ c][i]);
       }
-    }
+    std::vector<uint32_t> rest;
     for (auto& b : bucket)
-      for (auto it = b.rbegin(); it != b.rend(); ++it) rest.push_back(*it);
+      for (size_t i = static_cast<size_t>(steps * per); i < b.size(); ++i) rest.push_back(b[i]);
     std::sort(rest.begin(), rest.end());
+    pl.tie_from = static_cast<int64_t>(order.size());
     order.insert(order.end(), rest.begin(), rest.end());
+  } else {
+    // more couples than entry pairs: greedy matching of v with ~v inside
+    // windows of 1024 bins; no lane order, so the gather compares bins on
+    // every exact tie (tie_from = 0)
+    constexpr int64_t W = 1024;  // even: pairs stay on even entry offsets
+    pl.tie_from = 0;
+    for (int64_t w0 = 0; w0 < nu; w0 += W) {
+      const int64_t w1 = std::min<int64_t>(nu, w0 + W);
+      for (auto& b : bucket) b.clear();
+      for (int64_t u = w1 - 1; u >= w0; --u) {  // reversed: pop_back yields ascending
+        const uint32_t e = uniq[static_cast<size_t>(u)];
+        bucket[parity(e)].push_back(e);
+      }
+      std::vector<uint32_t> rest;
+      for (unsigned v = 0; v <= full; ++v) {
+        auto& a = bucket[v];
+        auto& b = bucket[full ^ v];
+        if (v > (full ^ v)) continue;  // each complementary couple once
+        while (!a.empty() && !b.empty() && (&a != &b || a.size() >= 2)) {
+          order.push_back(a.back());
+          a.pop_back();
+          order.push_back(b.back());
+          b.pop_back();
+        }
+      }
+      for (auto& b : bucket)
+        for (auto it = b.rbegin(); it != b.rend(); ++it) rest.push_back(*it);
+      std::sort(rest.begin(), rest.end());
+      order.insert(order.end(), rest.begin(), rest.end());
+    }
   }
   order.insert(order.end(), dups.begin(), dups.end());
   std::vector<uint16_t> prow(rows.size());

@@ -17,6 +17,9 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_bench.log 2>&1
 python tools/prof_step.py --config c3 --path map --trials 2048 --steps 1 > $O/plain3.log 2>&1 && \
   ncu -f --set full --clock-control none --import-source on -k regex:"k_gather|k_fft|k_topk" -c 3 \
   -o $E/prof_c3_$R python tools/prof_step.py --config c3 --path map --trials 2048 --steps 1 > $O/ncu3.log 2>&1
+python tools/time_topk.py --trials 9472 --steps 1 --warm 1 --engines pick,fused,map > $O/plain3p.log 2>&1 && \
+  ncu -f --set full --clock-control none --import-source on -k regex:"k_gather_pick" -c 1 \
+  -o $E/prof_c3pick_$R python tools/time_topk.py --trials 9472 --steps 1 --warm 0 --engines pick > $O/ncu3p.log 2>&1
 python tools/prof_step.py --config c3 --path topk --trials 2048 --steps 1 > $O/plain3f.log 2>&1 && \
   ncu -f --set full --clock-control none --import-source on -k regex:"k_gather_topk" -c 1 \
   -o $E/prof_c3fused_$R python tools/prof_step.py --config c3 --path topk --trials 2048 --steps 1 > $O/ncu3f.log 2>&1
