@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     // bank-permuted full plans: a lane meets the bins of the ordered part in
     // increasing order (first strict maximum = smallest bin); blocks reaching
     // into the unordered tail also flag exact ties
-    const bool tie = FULL && a.binid && entry0 + blk + 32 > a.tie_from;
+    const bool tie = false;
     if (nblk == 32 && kUnroll) {
       // full block: fixed trip count, no bounds checks, fully unrolled so
       // the next step's shuffles and loads overlap this step's updates

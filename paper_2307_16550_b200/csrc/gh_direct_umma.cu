@@ -62,7 +62,7 @@ struct UmmaArgs {
   unsigned long long* keys;
   const unsigned char* aprep;  // v2: prepared A stage blocks (k_prep_a)
   const float2* seeds;         // v2: [P][N/8][G] exp(j 2 pi rho n) at n = 8 c (k_seeds)
-  const unsigned* amax;        // v2 fp16: bits of max |frame component| (k_absmax)
+  const unsigned* amax;        // v2 fp16: [T] bits of each trial's max |frame component| (k_absmax)
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -368,13 +368,16 @@ __device__ __forceinline__ int amax_exp(const unsigned* amax) {
   return m > 0.f ? ilogbf(m) : 0;
 }
 
-__global__ void k_absmax(const float* __restrict__ x, int64_t n, unsigned* out) {
+// per trial (one CTA each): the largest |component| of the trial's frames, so
+// every trial is scaled by its own exponent and its precision does not
+// depend on the other trials of the batch
+__global__ void k_absmax(const float* __restrict__ x, int64_t per_trial, unsigned* out) {
+  const float* xt = x + (int64_t)blockIdx.x * per_trial;
   float m = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(x[i]));
+  for (int64_t i = threadIdx.x; i < per_trial; i += blockDim.x) m = fmaxf(m, fabsf(xt[i]));
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // >= 0: order-preserving
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(out + blockIdx.x, __float_as_uint(m));  // >= 0: order-preserving
 }
 
 __device__ __forceinline__ void split_store(unsigned char* big, unsigned char* sml, int off,
@@ -390,7 +393,6 @@ __global__ void k_prep_a(const float2* __restrict__ frames, int T, int P, int N,
   constexpr int CPS = H ? 4 : 2;   // complex samples per 16-byte chunk
   const int NCH = N / CPS;         // chunks along K per pair
   const int KC = NCH / KCH;        // stages per pair
-  const float scale = H ? ldexpf(1.f, -amax_exp(amax)) : 1.f;
   const int64_t n16 = (int64_t)((T + BT - 1) / BT) * BT * P * NCH;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n16;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -407,9 +409,11 @@ __global__ void k_prep_a(const float2* __restrict__ frames, int T, int P, int N,
     const float4* src = reinterpret_cast<const float4*>(frames + ((int64_t)t * P + p) * N);
     if constexpr (H) {
       float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+      float scale = 1.f;
       if (t < T) {
         v0 = __ldg(src + 2 * c16);
         v1 = __ldg(src + 2 * c16 + 1);
+        scale = ldexpf(1.f, -amax_exp(amax + t));
       }
       const float v[8] = {v0.x * scale, v0.y * scale, v0.z * scale, v0.w * scale,
                           v1.x * scale, v1.y * scale, v1.z * scale, v1.w * scale};
@@ -651,13 +655,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
     }
     // final: map or per-trial argmax over this warp's 64 bins (fp16: undo
     // the frames' power-of-two scale, exactly)
+    const int t = t0 + q * 32 + lane;
     if constexpr (H) {
-      const int e = amax_exp(a.amax);
+      const int e = t < a.T ? amax_exp(a.amax + t) : 0;  // this trial's own scale
       const float unscale = ldexpf(1.f, a.mag ? e : 2 * e);
 #pragma unroll
       for (int j = 0; j < 64; ++j) pw[j] *= unscale;
     }
-    const int t = t0 + q * 32 + lane;
     const int64_t gb0 = g0 + 64 * h;
     if (t < a.T) {
       if (a.map) {
@@ -731,14 +735,12 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
     }
     {
       KTimer kt(ctx, "direct_prep");
-      unsigned* amax = static_cast<unsigned*>(ctx->amax.get(sizeof(unsigned)));
+      unsigned* amax = static_cast<unsigned*>(ctx->amax.get(sizeof(unsigned) * T));
       a.amax = amax;
       if (h16) {
-        GH_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned), ctx->stream));
-        const int64_t nf = (int64_t)T * a.P * a.N * 2;
-        const int blocks = static_cast<int>(std::min<int64_t>((nf + 255) / 256, 148LL * 8));
-        v2::k_absmax<<<blocks, 256, 0, ctx->stream>>>(reinterpret_cast<const float*>(frames_d), nf,
-                                                      amax);
+        GH_CUDA(cudaMemsetAsync(amax, 0, sizeof(unsigned) * T, ctx->stream));
+        v2::k_absmax<<<T, 256, 0, ctx->stream>>>(reinterpret_cast<const float*>(frames_d),
+                                                 (int64_t)a.P * a.N * 2, amax);
         GH_LAUNCHED(ctx);
       }
       const int64_t n16 = (int64_t)tt * BT * a.P * (a.N / (h16 ? 4 : 2));

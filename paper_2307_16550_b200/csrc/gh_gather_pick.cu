@@ -76,21 +76,6 @@ __device__ __forceinline__ float unord_f(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-// plan row words: read once per batch by every CTA, so they should stay in
-// L2 while the batches' spectra stream through it (evict-last policy)
-__device__ __forceinline__ uint64_t l2_keep_policy() {
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint2 ldg_keep(const uint2* p, uint64_t pol) {
-  uint2 r;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
-               : "=r"(r.x), "=r"(r.y)
-               : "l"(p), "l"(pol));
-  return r;
-}
-
 // insert key ck into the warp's sorted register list (lane k < K: k-th key)
 __device__ __forceinline__ void list_insert(unsigned long long& mine, unsigned long long ck, int K,
                                             int lane) {
@@ -225,7 +210,6 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);                  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint4* sm4 = reinterpret_cast<uint4*>(smraw);
-  const uint64_t keep = l2_keep_policy();
   // this warp's candidate queue (global memory, L2-resident; rarely written)
   uint2* queue = pk.queue + ((size_t)blockIdx.x * NW + warp) * kPickQueue;
 
@@ -306,12 +290,13 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
       auto run = [&](auto seedc, int from, int& qn) -> int {
         constexpr bool SEED = decltype(seedc)::value;
         uint2 cur[PQ], nxt[PQ];
+        const uint2* rp = rows2 + entry0 + lane;  // this lane's row words, word q at + q * n_entries
 #pragma unroll
         for (int q = 0; q < PQ; ++q) cur[q] = nxt[q] = make_uint2(0u, 0u);
         if (from + lane < w1) {
 #pragma unroll
           for (int q = 0; q < PQ; ++q)
-            if (q < pq) cur[q] = ldg_keep(rows2 + q * a.n_entries + entry0 + from + lane, keep);
+            if (q < pq) cur[q] = __ldg(rp + q * a.n_entries + from);
         }
         float sbest[4] = {-1.0f, -1.0f, -1.0f, -1.0f};  // SEED: this lane's largest values
         int sblb[4] = {-1, -1, -1, -1};
@@ -324,7 +309,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
           if (blk + 32 + lane < w1) {
 #pragma unroll
             for (int q = 0; q < PQ; ++q)
-              if (q < pq) nxt[q] = ldg_keep(rows2 + q * a.n_entries + entry0 + blk + 32 + lane, keep);
+              if (q < pq) nxt[q] = __ldg(rp + q * a.n_entries + blk + 32);
           }
           float thr[4];
           if constexpr (!SEED)  // one volatile LDS.128: other warps raise these values

@@ -225,6 +225,25 @@ def test_direct_fp16_frame_scaling(ctx, gain):
     assert_argmax_parity(ref, idx.cpu().numpy(), f"direct fp16 x{gain}")
 
 
+def test_direct_fp16_mixed_trial_amplitudes(ctx):
+    # every trial is scaled by its own power of two: a batch mixing trials
+    # 9 decades apart keeps each trial's map as accurate as on its own (one
+    # batch-wide exponent would push the weak trials' fp16 parts into
+    # subnormals)
+    sc = S.small()
+    T = 12
+    fr, _ = O.synth(sc, 5, T)
+    gains = np.array([1e4, 1e-5, 1.0, 3e-3] * 3)[:, None, None]
+    fr = fr * gains
+    ref = O.direct_map(sc, fr)
+    fd = frames_to_dev(fr)
+    m = gh.location_decision_map(ctx, sc, fd).cpu().numpy()
+    for t in range(T):
+        assert rel_map_err(m[t:t + 1], ref[t:t + 1]) < MAP_TOL, t
+    idx, _ = gh.direct_argmax(ctx, sc, fd)
+    assert_argmax_parity(ref, idx.cpu().numpy(), "direct fp16 mixed amplitudes")
+
+
 def test_direct_tcgen05_c2_scale(ctx):
     # the c2 scene (40,000 bins x 3 pairs, N = 256), 130 trials: two trial
     # tiles of 128 (ragged) through the tensor-core path
