@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "gh_gather_common.cuh"
 #include "gh_internal.cuh"
@@ -201,13 +202,17 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
     best[i] = -1.0f;
     blb[i] = -1;
   }
-  // full plans: 32-bin multiples (bank-complementary entry pairs stay on
-  // even offsets); tiled plans: warp-step multiples, so small tiles still
-  // spread over every warp
-  constexpr int64_t kRound = FULL ? 32 : BPW;
+  // full plans: 32-entry blocks dealt round-robin to the warps (bank-
+  // complementary entry pairs stay on even offsets, a lane still meets its
+  // entries in increasing order, and the plan's tail blocks spread over all
+  // warps instead of making the last one the straggler); tiled plans:
+  // contiguous runs in warp-step multiples, so small tiles still spread over
+  // every warp
+  constexpr int64_t kRound = BPW;
   const int64_t per_warp = ((nb + NW - 1) / NW + kRound - 1) / kRound * kRound;
-  const int64_t w0 = warp * per_warp;
-  const int64_t w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
+  const int64_t w0 = FULL ? warp * 32 : warp * per_warp;
+  const int64_t w1 = FULL ? nb : (w0 + per_warp < nb ? w0 + per_warp : nb);
+  constexpr int64_t kBlockStep = FULL ? NW * 32 : 32;
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint2 cur[PQ], nxt[PQ];
@@ -227,19 +232,29 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
   }
   mbar_wait(&stage_bar, phase);
   phase ^= 1u;
-  for (int64_t blk = w0; blk < w1; blk += 32) {
-    if (blk + 32 + lane < w1) {
+  // The warp's blocks in two runs of the same loop: the plan's lane-ordered
+  // part (TIE = false: exactly the plain gather loop) and, on bank-permuted
+  // full plans, its ascending tail from a.tie_from on (TIE = true: the same
+  // step plus an equality test that flags exact ties for tail_scan). The
+  // row-word prefetch runs across the seam.
+  auto blocks = [&](auto tiec, int64_t b0, int64_t b1) -> int64_t {
+  constexpr bool TIE = decltype(tiec)::value;
+  int64_t blk = b0;
+  for (; blk < b1; blk += kBlockStep) {
+    unsigned tied = 0u;  // TIE: this lane's trials that met an exact tie in the block
+    if (blk + kBlockStep + lane < w1) {
       if constexpr (CP) {
-        nxt[0].x = __ldg(a.crow + entry0 + blk + 32 + lane);
+        nxt[0].x = __ldg(a.crow + entry0 + blk + kBlockStep + lane);
       } else {
 #pragma unroll
         for (int q = 0; q < PQ; ++q)
-          if (q < pq) nxt[q] = __ldg(rows2 + q * a.n_entries + entry0 + blk + 32 + lane);
+          if (q < pq)
+            nxt[q] = __ldg(rows2 + q * a.n_entries + entry0 + blk + kBlockStep + lane);
       }
     }
     const int nblk = w1 - blk < 32 ? (int)(w1 - blk) : 32;
     // one step: lane group `sub` handles bin j = s * BPW + sub of the block
-    auto step = [&](int s, bool check, bool tie) {
+    auto step = [&](int s, bool check) {
       const int j = s * BPW + sub;
       const int64_t lb = blk + (!check || j < nblk ? j : 0);
       float2 acc[2];
@@ -293,39 +308,43 @@ __global__ void __launch_bounds__(gather_threads<K3, FULL>(), 1) k_gather(Gather
             if (vals[i] > best[i]) {
               best[i] = vals[i];
               blb[i] = (int)lb;
-            } else if (FULL && tie && vals[i] == best[i]) {
+            } else if (TIE && vals[i] == best[i]) {
               // an entry of the plan's unordered tail ties with the lane's
-              // running maximum: flag the trial, the item's epilogue settles
-              // it (tail_scan); rare, and only tail blocks test for it
-              atomicOr(&tie_mask, 1u << (v * TPL + i));
+              // running maximum: note the trial, the item's epilogue settles
+              // it (tail_scan); only tail blocks test for it
+              tied |= 1u << i;
             }
           }
         }
       }
     };
     constexpr bool kUnroll = !K3 && PC > 0 && PC <= 16;
-    // bank-permuted full plans: a lane meets the bins of the ordered part in
-    // increasing order (first strict maximum = smallest bin); blocks reaching
-    // into the unordered tail also flag exact ties
-    const bool tie = FULL && a.binid && entry0 + blk + 32 > a.tie_from;
     if (nblk == 32 && kUnroll) {
       // full block: fixed trip count, no bounds checks, fully unrolled so
       // the next step's shuffles and loads overlap this step's updates
-      if (!tie) {
 #pragma unroll
-        for (int s = 0; s < 32 / BPW; ++s) step(s, false, false);
-      } else {
-#pragma unroll
-        for (int s = 0; s < 32 / BPW; ++s) step(s, false, true);
-      }
+      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
     } else if (nblk == 32) {
 #pragma unroll 1
-      for (int s = 0; s < 32 / BPW; ++s) step(s, false, tie);
+      for (int s = 0; s < 32 / BPW; ++s) step(s, false);
     } else {
-      for (int s = 0; s * BPW < nblk; ++s) step(s, true, tie);
+      for (int s = 0; s * BPW < nblk; ++s) step(s, true);
     }
+    if constexpr (TIE)
+      if (tied) atomicOr(&tie_mask, tied << (v * TPL));
 #pragma unroll
     for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
+  }
+  return blk;
+  };
+  if constexpr (FULL && !K3 && !MAPMODE) {
+    // tie_from and entry0 are multiples of 32, like every block start
+    int64_t wa = a.binid ? a.tie_from - entry0 : w1;
+    wa = wa > w1 ? w1 : wa;
+    const int64_t seam = blocks(std::false_type{}, w0, wa);  // the warp's first tail block
+    blocks(std::true_type{}, seam, w1);
+  } else {
+    blocks(std::false_type{}, w0, w1);
   }
   if constexpr (!MAPMODE) {
     // exact ties go to the smaller bin: compare global bins (entry order is
