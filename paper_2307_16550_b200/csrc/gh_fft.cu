@@ -603,8 +603,15 @@ __device__ __forceinline__ void fixed_passes(float4* buf, const float2* ptw) {
 // epilogue kinds of the fixed kernel (compile time)
 enum FxOut { FX_NATURAL = 0, FX_REAL = 1, FX_COMPLEX = 2 };
 
+// c3 (N = 1024, os = 4, one row pair): capped at 128 registers (8 bytes of spills)
+// so two CTAs share an SM (102 KB of shared memory each); uncapped it takes 156
+// registers and runs one CTA of 8 warps per SM
+template <int LN, int LOS, int LP>
+constexpr int fixed_min_ctas() { return LN == 10 && LOS == 2 && LP == 0 ? 2 : 1; }
+
 template <int LN, int LOS, int LP, bool SYNTH, int KIND>
-__global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS) k_fft_fixed(FftArgs a) {
+__global__ void __launch_bounds__(Fx<LN, LOS, LP>::THREADS, fixed_min_ctas<LN, LOS, LP>())
+    k_fft_fixed(FftArgs a) {
   using F = Fx<LN, LOS, LP>;
   constexpr int N = F::N, M = F::M, PAIRS = F::PAIRS, ROWS = F::ROWS, NT = F::THREADS;
   extern __shared__ float4 smem4[];
