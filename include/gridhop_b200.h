@@ -116,6 +116,12 @@ int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
  * its loop and candidates verified against the table and spectra (no maps).
  * All engines return identical bins and values. */
 int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl);
+/* Debug builds of the hand-rolled pipelines (compute-sanitizer's stand-in):
+ * with on != 0, kernels that have a bounds-tested instantiation run it — the
+ * top-K pick gather tests every staged shared-memory offset, window extent,
+ * candidate-queue slot and table / spectra row it touches — and a violation
+ * fails the call with GH_ERUNTIME. Same results, slower, synchronous. */
+int gh_ctx_set_debug_checks(gh_ctx* ctx, int32_t on);
 /* Diagnostics: measured shared-memory (LSU) read bandwidth of the device,
  * GB/s, all SMs — the roofline denominator of the gather kernel. */
 int gh_measure_smem_peak(gh_ctx* ctx, double* gbps);

@@ -141,6 +141,7 @@ def lib() -> C.CDLL:
             "gh_measure_smem_peak": (C.c_int, [vp, P(f64)]),
             "gh_ctx_set_direct_impl": (C.c_int, [vp, i32]),
             "gh_ctx_set_topk_impl": (C.c_int, [vp, i32]),
+            "gh_ctx_set_debug_checks": (C.c_int, [vp, i32]),
             "gh_table_build": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, P(vp)]),
             "gh_table_upload": (C.c_int, [vp, P(CWave), P(CGrid), i32, vp, vp, P(vp)]),
             "gh_table_build_shard": (C.c_int, [vp, P(CWave), P(CGrid), i32, i32, i32, i32, P(vp)]),
@@ -266,6 +267,11 @@ class Context:
         no maps), 'fused' (halo tiles, values in shared memory) or 'map'
         (map-mode gather, then k_topk_localmax on the maps)."""
         _check(lib().gh_ctx_set_topk_impl(self.h, {"auto": 0, "fused": 1, "map": 2, "pick": 3}[impl]))
+
+    def set_debug_checks(self, on: bool) -> None:
+        """Run the bounds-tested kernel builds where one exists (the top-K pick
+        gather); a violation raises GridhopRuntimeError."""
+        _check(lib().gh_ctx_set_debug_checks(self.h, int(on)))
 
     def set_direct_impl(self, impl: str) -> None:
         """'tcgen05' (default: warp-specialised 3xFP16 tensor-core pipeline),

@@ -757,6 +757,14 @@ int gh_ctx_set_topk_impl(gh_ctx* ctx, int32_t impl) {
   });
 }
 
+int gh_ctx_set_debug_checks(gh_ctx* ctx, int32_t on) {
+  return guarded([&] {
+    auto* c = reinterpret_cast<gh::Ctx*>(ctx);
+    if (!c) fail(GH_EINVAL, "ctx: null argument");
+    c->debug_checks = on != 0;
+  });
+}
+
 int gh_ctx_set_timing(gh_ctx* ctx, int32_t on) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);

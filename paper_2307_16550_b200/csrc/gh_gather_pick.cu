@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <type_traits>
 
 #include "gh_gather_common.cuh"
@@ -42,6 +43,11 @@ constexpr int kPickThreads = 768;
 constexpr int kPickMaxK = 8;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kPickQueue = 1024;  // candidate entries per warp queue (global memory)
+// CHECK builds (gh_ctx_set_debug_checks): every staged-window offset, window
+// extent, queue slot and table / spectra index of the kernel is tested and a
+// violation sets one of these bits (compute-sanitizer is closed on this pool)
+constexpr unsigned kViolSmemOffset = 1u, kViolQueue = 2u, kViolWindow = 4u, kViolTable = 8u,
+                   kViolSpectra = 16u;
 
 struct PickArgs {
   int K;
@@ -50,6 +56,8 @@ struct PickArgs {
   float* out_val;         // [T][K]
   unsigned* counter;      // batch work counter, zeroed by the launcher
   uint2* queue;           // [CTAs][warps][kPickQueue] candidate queues
+  unsigned* viol;         // CHECK builds: bounds-violation mask (see kViol*)
+  unsigned smem_bytes;    // CHECK builds: dynamic shared memory of the launch
   int axis3;              // 1: 3-D lattice (26 neighbours, layers along z), 0: 2-D (layers along y)
   int lat_lo, lat_hi;     // layers of the table (a shard holds [lat_lo, lat_hi))
   int core_lo, core_hi;   // layers whose maxima are reported
@@ -66,6 +74,8 @@ struct __align__(16) PickShared {
   int64_t bin0;
   const uint32_t* idx;
   const float* spec;  // the batch's spectra [P][M][8]
+  unsigned* viol;     // CHECK builds, else null
+  int64_t G;          // bins of the table (CHECK builds)
 };
 
 __device__ __forceinline__ uint32_t ord_f(float v) {
@@ -124,9 +134,14 @@ __device__ __noinline__ void drain_candidates(const uint2* q, int qn, const Tile
     const int x = cx + dx, y = cy + dy, z = cz + dz;
     const int nlay = d3 ? z : y;
     bool ok = true;
-    if (want && tester && x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz &&
-        nlay >= sh->lat_lo && nlay < sh->lat_hi) {
-      const int64_t nb = x + (int64_t)nx * (y + (int64_t)ny * z);
+    bool test = want && tester && x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz &&
+                nlay >= sh->lat_lo && nlay < sh->lat_hi;
+    const int64_t nb = x + (int64_t)nx * (y + (int64_t)ny * z);
+    if (test && sh->viol && (nb - sh->bin0 < 0 || nb - sh->bin0 >= sh->G)) {
+      atomicOr(sh->viol, kViolTable);
+      test = false;
+    }
+    if (test) {
       const uint32_t* ip = sh->idx + (nb - sh->bin0) * P;
       const float* sp = sh->spec + ts;
       float sum = 0.f;
@@ -144,6 +159,12 @@ __device__ __noinline__ void drain_candidates(const uint2* q, int qn, const Tile
 #pragma unroll
           for (int u = 0; u < 16; ++u) row[u] = p0 + u < P ? __ldg(ip + p0 + u) : 0u;
         }
+        if (sh->viol)
+          for (int u = 0; u < 16; ++u)
+            if (p0 + u < P && row[u] >= (uint32_t)M) {
+              atomicOr(sh->viol, kViolSpectra);
+              row[u] = 0u;
+            }
 #pragma unroll
         for (int u = 0; u < 16; ++u)
           zv[u] = p0 + u < P ? __ldg(sp + ((int64_t)(p0 + u) * M + row[u]) * TB) : 0.f;
@@ -186,8 +207,9 @@ __device__ __noinline__ void drain_candidates(const uint2* q, int qn, const Tile
   }
 }
 
-// PC: compile-time pair count (0 = runtime, at most 4 * PQ)
-template <int PC, int PQ>
+// PC: compile-time pair count (0 = runtime, at most 4 * PQ); CHECK: bounds
+// tests on every staged offset, window, queue slot and table index
+template <int PC, int PQ, bool CHECK = false>
 __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, PickArgs pk) {
   constexpr int TB = 8, ES = 4, L = 2, BPW = 16, NW = kPickThreads / 32;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -202,6 +224,8 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
     sh.lat_lo = pk.lat_lo, sh.lat_hi = pk.lat_hi, sh.core_lo = pk.core_lo, sh.core_hi = pk.core_hi;
     sh.bin0 = a.bin0;
     sh.idx = pk.idx;
+    sh.viol = CHECK ? pk.viol : nullptr;
+    sh.G = a.G;
   }
   uint32_t phase = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -254,6 +278,10 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         __syncwarp();
         for (int p = lane; p < P; p += 32) {
           const int4 w = __ldg(&win[p]);
+          if constexpr (CHECK)
+            if (w.x < 0 || w.x >= a.M || w.y < 0 || w.y > a.M || w.z < 0 ||
+                (size_t)(w.z + w.y) * 16u * L > pk.smem_bytes)
+              atomicOr(pk.viol, kViolWindow);
           const uint4* src = spec + (int64_t)p * a.M * L;
           uint4* dst = sm4 + (int64_t)w.z * L;
           for (int r = 0, gi = w.x; r < w.y; gi = 0) {  // base in [0, M): split where it wraps
@@ -333,6 +361,9 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
               for (int u = 0; u < 4; ++u) {
                 const int p = 4 * q + u;
                 if (PC ? p >= PC : p >= a.P) break;
+                if constexpr (CHECK)
+                  if (live && (size_t)(o[u] + L) * 16u > (size_t)tdp->rows * 16u * L)
+                    atomicOr(pk.viol, kViolSmemOffset);
                 accumulate<TB, false, false, L>(smv, o[u], nullptr, acc, p == 0);
               }
             }
@@ -375,6 +406,11 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   const unsigned m = __ballot_sync(kFullMask, cand[i]);
+                  if constexpr (CHECK)
+                    if (qn + __popc(m) > kPickQueue) {
+                      atomicOr(pk.viol, kViolQueue);
+                      continue;
+                    }
                   if (cand[i])
                     queue[qn + __popc(m & ((1u << lane) - 1u))] =
                         make_uint2((unsigned)lb | (unsigned)(v * 4 + i) << 28,
@@ -493,9 +529,26 @@ void launch_gather_pick(Ctx* ctx, Table* t, const void* spec_d, int T, int K, in
     GH_LAUNCHED(ctx);
   };
   const int pq = pl.p4 / 4;
-  if (t->P == 16) go(k_gather_pick<16, 4>);
-  else if (pq <= 1) go(k_gather_pick<0, 1>);
-  else go(k_gather_pick<0, 4>);
+  if (!ctx->debug_checks) {
+    if (t->P == 16) go(k_gather_pick<16, 4>);
+    else if (pq <= 1) go(k_gather_pick<0, 1>);
+    else go(k_gather_pick<0, 4>);
+    return;
+  }
+  // debug build of the same kernel: every shared-memory offset, window,
+  // queue slot and table index bounds-tested; synchronous report
+  pk.viol = reinterpret_cast<unsigned*>(scratch + 128);
+  pk.smem_bytes = static_cast<unsigned>(smem);
+  GH_CUDA(cudaMemsetAsync(pk.viol, 0, sizeof(unsigned), ctx->stream));
+  if (t->P == 16) go(k_gather_pick<16, 4, true>);
+  else if (pq <= 1) go(k_gather_pick<0, 1, true>);
+  else go(k_gather_pick<0, 4, true>);
+  unsigned mask = 0;
+  GH_CUDA(cudaMemcpyAsync(&mask, pk.viol, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  GH_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (mask)
+    fail(GH_ERUNTIME, "gather pick: bounds check failed (mask " + std::to_string(mask) +
+                          ": 1 staged offset, 2 queue slot, 4 window, 8 table row, 16 spectra row)");
 }
 
 }  // namespace gh

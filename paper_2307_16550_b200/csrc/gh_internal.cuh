@@ -94,6 +94,8 @@ struct Ctx {
   // deferred campaign-synthesis error flag (window / degenerate geometry)
   int* synth_flag_d = nullptr;
   bool synth_pending = false;
+  // bounds-tested kernel builds where one exists (gh_ctx_set_debug_checks)
+  bool debug_checks = false;
 };
 
 // Records events around one launch when ctx->timing is set.

@@ -160,3 +160,25 @@ def test_auto_engine_takes_pick_on_large_batches(ctx, fused_engine):
     mi, mv = gh.campaign_hop_topk(ctx, t, sc, 0, T, k)
     assert np.array_equal(ai.cpu().numpy(), mi.cpu().numpy())
     assert np.array_equal(av.cpu().numpy(), mv.cpu().numpy())
+
+
+def test_pick_engine_bounds_checked_build(ctx, fused_engine):
+    # compute-sanitizer's stand-in: the CHECK instantiation of k_gather_pick
+    # tests every staged shared-memory offset, window extent, queue slot and
+    # table / spectra row; it must run clean and return the same lists
+    if fused_engine != "pick":
+        pytest.skip("the bounds-tested build belongs to the pick engine")
+    for sc, T, k in ((c3_sub(), 37, 5), (c3_sub(120, 98), 9, 4), (S.baseline("c3"), 19, 5)):
+        t = gh.precompute_hop_table(ctx, sc)
+        fr, _ = O.synth(sc, 21, T)
+        fd = frames_to_dev(fr)
+        pi, pv = gh.hop_topk(ctx, t, fd, k)
+        ctx.set_debug_checks(True)
+        try:
+            ci, cv = gh.hop_topk(ctx, t, fd, k)
+            zi, _ = gh.hop_topk(ctx, t, torch.zeros_like(fd), k)  # every bin a candidate
+        finally:
+            ctx.set_debug_checks(False)
+        assert np.array_equal(ci.cpu().numpy(), pi.cpu().numpy())
+        assert np.array_equal(cv.cpu().numpy(), pv.cpu().numpy())
+        assert (zi.cpu().numpy()[:, 0] == 0).all()
