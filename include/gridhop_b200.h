@@ -106,7 +106,10 @@ int gh_ctx_reset_timing(gh_ctx* ctx);
  * power-of-two-scaled frames), warp-specialised pipeline (default); 1 =
  * CUDA-core fp32 contraction (the reference path the tensor-core kernels are
  * checked and timed against); 2 = single-stage tcgen05 3xTF32 kernel (v1);
- * 3 = the warp-specialised pipeline in 3xTF32 (kind::tf32). */
+ * 3 = the warp-specialised pipeline in 3xTF32 (kind::tf32); 4 = the same
+ * pipeline with one fp16 MMA per K step (1xFP16 fast mode: a third of the
+ * tensor work; fp16 operands leave the c2 maps ~8e-5 of their maximum off,
+ * marginal against the 1e-4 parity bar, so it is never the default). */
 int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
 /* Top-K local-maximum engine (BASELINE c3): 0 = auto (engine 3 where the
  * table's plan admits it — tiled K = 1 plans of at most 16 pairs — and the

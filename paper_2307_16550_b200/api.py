@@ -276,9 +276,12 @@ class Context:
     def set_direct_impl(self, impl: str) -> None:
         """'tcgen05' (default: warp-specialised 3xFP16 tensor-core pipeline),
         'tcgen05_tf32' (the same pipeline in 3xTF32), 'tcgen05_v1' (single-stage
-        3xTF32 kernel) or 'simt' (CUDA-core fp32)."""
+        3xTF32 kernel), 'simt' (CUDA-core fp32) or 'tcgen05_fast' (1xFP16: one
+        MMA per K step; c2 maps ~8e-5 of their maximum off, marginal against
+        the 1e-4 bar, not the default)."""
         _check(lib().gh_ctx_set_direct_impl(
-            self.h, {"tcgen05": 0, "simt": 1, "tcgen05_v1": 2, "tcgen05_tf32": 3}[impl]))
+            self.h, {"tcgen05": 0, "simt": 1, "tcgen05_v1": 2, "tcgen05_tf32": 3,
+                     "tcgen05_fast": 4}[impl]))
 
     def smem_peak_gbps(self) -> float:
         v = C.c_double()

@@ -737,10 +737,10 @@ int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl) {
   return guarded([&] {
     auto* c = reinterpret_cast<gh::Ctx*>(ctx);
     if (!c) fail(GH_EINVAL, "ctx: null argument");
-    if (impl < 0 || impl > 3)
+    if (impl < 0 || impl > 4)
       fail(GH_EINVAL,
-           "ctx: direct impl must be 0 (tcgen05 3xFP16), 1 (simt), 2 (tcgen05 v1) or 3 (tcgen05 "
-           "3xTF32)");
+           "ctx: direct impl must be 0 (tcgen05 3xFP16), 1 (simt), 2 (tcgen05 v1), 3 (tcgen05 "
+           "3xTF32) or 4 (tcgen05 1xFP16 fast mode)");
     c->direct_impl = impl;
   });
 }

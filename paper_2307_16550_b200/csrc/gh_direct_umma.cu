@@ -63,6 +63,7 @@ struct UmmaArgs {
   const unsigned char* aprep;  // v2: prepared A stage blocks (k_prep_a)
   const float2* seeds;         // v2: [P][N/8][G] exp(j 2 pi rho n) at n = 8 c (k_seeds)
   const unsigned* amax;        // v2 fp16: [T] bits of each trial's max |frame component| (k_absmax)
+  int fast;                    // v2: 1 = one MMA per K step (hi * hi only): the 1xFP16 fast mode
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -625,8 +626,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_direct_umma2(UmmaArgs a) {
               const uint64_t dbb = umma_desc(bb + 2 * k * LBOB, LBOB, 128);
               const uint64_t dbs = umma_desc(bs + 2 * k * LBOB, LBOB, 128);
               mma<H>(tmem, dab, dbb, (kc0 > 0 || k > 0) ? 1u : 0u);
-              mma<H>(tmem, dab, dbs, 1u);
-              mma<H>(tmem, das, dbb, 1u);
+              if (!a.fast) {  // the 3x split's cross terms (fast mode: hi * hi only)
+                mma<H>(tmem, dab, dbs, 1u);
+                mma<H>(tmem, das, dbb, 1u);
+              }
             }
             mma_commit(&empty[s]);
           }
@@ -711,9 +714,10 @@ void direct_map_umma(Ctx* ctx, const double* txrx_d, const gh_wave* w, const gh_
   a.keys = keys_d;
   if (a.P > kMaxPairs) fail(GH_EINVAL, "direct: at most 64 TX-RX pairs");
   if (a.N % 2) fail(GH_EINVAL, "direct: n_samples must be even");
-  if (ctx->direct_impl == 0 || ctx->direct_impl == 3) {
+  if (ctx->direct_impl == 0 || ctx->direct_impl == 3 || ctx->direct_impl == 4) {
     // 0: 3xFP16 (kind::f16), 3: 3xTF32 (kind::tf32); both warp-specialised
-    const bool h16 = ctx->direct_impl == 0;
+    const bool h16 = ctx->direct_impl != 3;
+    a.fast = ctx->direct_impl == 4;
     const int sps = h16 ? 32 : 16;
     if (a.N % sps)
       fail(GH_EINVAL, std::string("direct: n_samples must be a multiple of ") + std::to_string(sps));
