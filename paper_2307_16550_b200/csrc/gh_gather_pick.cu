@@ -10,7 +10,7 @@
 //
 // One CTA owns a batch of 8 trials for the whole grid: it walks the plan's
 // tiles one after the other (stage the tile's range windows by TMA bulk
-// copies, gather with all 24 warps) and keeps the batch's per-trial top-K
+// copies, gather with all 20 warps) and keeps the batch's per-trial top-K
 // key lists in shared memory. The gather loop itself only compares each
 // value with its trial's prune value — the K-th best local maximum found so
 // far, -1 until K are known — which is one FSETP per value, less than the
@@ -39,7 +39,10 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kPickThreads = 768;
+// 20 warps: 96 registers per thread, so the loop keeps three sets of row words
+// (this block and the next two) without spills; 24 warps (80 registers)
+// spilled loop invariants and ran 6 % slower, 16 warps 2 % slower
+constexpr int kPickThreads = 640;
 constexpr int kPickMaxK = 8;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr int kPickQueue = 1024;  // candidate entries per warp queue (global memory)
@@ -234,8 +237,9 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
   const int pq = PC ? (PC + 3) / 4 : (a.p4 >> 2);                  // uint2 words (4 pairs) per bin
   const uint2* rows2 = reinterpret_cast<const uint2*>(a.rows);
   uint4* sm4 = reinterpret_cast<uint4*>(smraw);
-  // this warp's candidate queue (global memory, L2-resident; rarely written)
-  uint2* queue = pk.queue + ((size_t)blockIdx.x * NW + warp) * kPickQueue;
+  // this warp's candidate queue (global memory, L2-resident; rarely written):
+  // its address is formed where it is used, not kept in registers
+  auto my_queue = [&]() { return pk.queue + ((size_t)blockIdx.x * NW + warp) * kPickQueue; };
 
   for (;;) {
     __syncthreads();  // the previous batch's lists are written out
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
                                                        (int64_t)tb * a.P * a.M * TB * ES);
 
     // Pass -1 seeds the prune values: tile 0 is gathered once keeping each
-    // warp's largest value per trial (the argmax update), and those 24 strip
+    // warp's largest value per trial (the argmax update), and those 20 strip
     // maxima per trial are verified and listed, so the K-th best of them
     // prunes from the first real step on (without it every bin is a
     // candidate until a trial has K maxima). Then every tile, tile 0 again.
@@ -317,14 +321,22 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
       // selects the per-bin action.
       auto run = [&](auto seedc, int from, int& qn) -> int {
         constexpr bool SEED = decltype(seedc)::value;
-        uint2 cur[PQ], nxt[PQ];
-        const uint2* rp = rows2 + entry0 + lane;  // this lane's row words, word q at + q * n_entries
+        uint2 cur[PQ], nxt[PQ], nx2[PQ];  // row words of this block and the next two
+        // this lane's row words: word q of entry e at rp[q * ne + e] (32-bit
+        // offsets: one base pointer stays live, not one per word)
+        const uint2* rp = rows2 + entry0 + lane;
+        const unsigned ne = (unsigned)a.n_entries;
 #pragma unroll
-        for (int q = 0; q < PQ; ++q) cur[q] = nxt[q] = make_uint2(0u, 0u);
+        for (int q = 0; q < PQ; ++q) cur[q] = nxt[q] = nx2[q] = make_uint2(0u, 0u);
         if (from + lane < w1) {
 #pragma unroll
           for (int q = 0; q < PQ; ++q)
-            if (q < pq) cur[q] = __ldg(rp + q * a.n_entries + from);
+            if (q < pq) cur[q] = __ldg(rp + (q * ne + (unsigned)from));
+        }
+        if (from + 32 + lane < w1) {
+#pragma unroll
+          for (int q = 0; q < PQ; ++q)
+            if (q < pq) nxt[q] = __ldg(rp + (q * ne + (unsigned)(from + 32)));
         }
         float sbest[4] = {-1.0f, -1.0f, -1.0f, -1.0f};  // SEED: this lane's largest values
         int sblb[4] = {-1, -1, -1, -1};
@@ -334,10 +346,10 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         int blk = from;
         for (; blk < w1; blk += 32) {
           if (qn > kPickQueue - 256) break;  // a block pushes at most 2 x 32 x 4 entries
-          if (blk + 32 + lane < w1) {
+          if (blk + 64 + lane < w1) {  // two blocks ahead: L2 latency under load
 #pragma unroll
             for (int q = 0; q < PQ; ++q)
-              if (q < pq) nxt[q] = __ldg(rp + q * a.n_entries + blk + 32);
+              if (q < pq) nx2[q] = __ldg(rp + (q * ne + (unsigned)(blk + 64)));
           }
           float thr[4];
           if constexpr (!SEED)  // one volatile LDS.128: other warps raise these values
@@ -412,7 +424,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
                       continue;
                     }
                   if (cand[i])
-                    queue[qn + __popc(m & ((1u << lane) - 1u))] =
+                    my_queue()[qn + __popc(m & ((1u << lane) - 1u))] =
                         make_uint2((unsigned)lb | (unsigned)(v * 4 + i) << 28,
                                    __float_as_uint(vv[i]));
                   qn += __popc(m);
@@ -427,7 +439,10 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
             for (int s = 0; s * BPW < nblk; ++s) step(s, true);
           }
 #pragma unroll
-          for (int q = 0; q < PQ; ++q) cur[q] = nxt[q];
+          for (int q = 0; q < PQ; ++q) {
+            cur[q] = nxt[q];
+            nxt[q] = nx2[q];
+          }
         }
         if constexpr (SEED) {
           // the warp's strip maximum per trial (lanes of equal v share trials)
@@ -444,7 +459,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
             const bool push = sub == 0 && sblb[i] >= 0 && tb * TB + v * 4 + i < a.T;
             const unsigned m = __ballot_sync(kFullMask, push);
             if (push)
-              queue[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(
+              my_queue()[qn + __popc(m & ((1u << lane) - 1u))] = make_uint2(
                   (unsigned)sblb[i] | (unsigned)(v * 4 + i) << 28, __float_as_uint(sbest[i]));
             qn += __popc(m);
           }
@@ -455,7 +470,7 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         int qn = 0;
         from = ti < 0 ? run(std::true_type{}, from, qn) : run(std::false_type{}, from, qn);
         __syncwarp();
-        if (qn) drain_candidates(queue, qn, tdp, &sh);
+        if (qn) drain_candidates(my_queue(), qn, a.tiles + tile, &sh);
         if (from >= w1) break;
       }
       phase ^= 1u;

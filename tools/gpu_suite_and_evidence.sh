@@ -1,4 +1,4 @@
-# session-4 state check: full GPU suite, then the round-2 evidence run
+# gpurun -- bash tools/gpu_suite_and_evidence.sh: the full GPU suite, then the round-2 evidence run
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
