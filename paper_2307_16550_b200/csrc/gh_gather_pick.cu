@@ -310,9 +310,12 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
           }
         }
       }
-      const int per_warp = ((nb + NW - 1) / NW + BPW - 1) / BPW * BPW;
-      const int w0 = warp * per_warp < nb ? warp * per_warp : nb;
-      const int w1 = w0 + per_warp < nb ? w0 + per_warp : nb;
+      // 32-entry blocks dealt round-robin to the warps: the bins of a peak's
+      // main lobe (a few adjacent blocks, many candidates) spread over
+      // several warps' queues instead of making one warp the tile's straggler
+      constexpr int kStride = NW * 32;
+      const int w0 = warp * 32 < nb ? warp * 32 : nb;
+      const int w1 = nb;
       const bool blk24 = tdp->blk == 1 + 1 + (2 << 2);  // 2 x 4 x 1 entry blocks
       // One run over the warp's entries from block `from` until its end or
       // until the queue could overflow in the next block; returns where to
@@ -333,10 +336,10 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
           for (int q = 0; q < PQ; ++q)
             if (q < pq) cur[q] = __ldg(rp + (q * ne + (unsigned)from));
         }
-        if (from + 32 + lane < w1) {
+        if (from + kStride + lane < w1) {
 #pragma unroll
           for (int q = 0; q < PQ; ++q)
-            if (q < pq) nxt[q] = __ldg(rp + (q * ne + (unsigned)(from + 32)));
+            if (q < pq) nxt[q] = __ldg(rp + (q * ne + (unsigned)(from + kStride)));
         }
         float sbest[4] = {-1.0f, -1.0f, -1.0f, -1.0f};  // SEED: this lane's largest values
         int sblb[4] = {-1, -1, -1, -1};
@@ -344,12 +347,12 @@ __global__ void __launch_bounds__(kPickThreads, 1) k_gather_pick(GatherArgs a, P
         // of the same tile finds the phase complete)
         mbar_wait(&stage_bar, phase);
         int blk = from;
-        for (; blk < w1; blk += 32) {
+        for (; blk < w1; blk += kStride) {
           if (qn > kPickQueue - 256) break;  // a block pushes at most 2 x 32 x 4 entries
-          if (blk + 64 + lane < w1) {  // two blocks ahead: L2 latency under load
+          if (blk + 2 * kStride + lane < w1) {  // two blocks ahead: L2 latency under load
 #pragma unroll
             for (int q = 0; q < PQ; ++q)
-              if (q < pq) nx2[q] = __ldg(rp + (q * ne + (unsigned)(blk + 64)));
+              if (q < pq) nx2[q] = __ldg(rp + (q * ne + (unsigned)(blk + 2 * kStride)));
           }
           float thr[4];
           if constexpr (!SEED)  // one volatile LDS.128: other warps raise these values
