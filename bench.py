@@ -56,7 +56,7 @@ def peaks() -> dict:
 # gather instantiation per BASELINE config: its ncu --set full capture in
 # profiles/ supplies roofline.traffic (DRAM read + write per launch)
 GATHER_KERNEL = {"c1": "k_gather<16, 0, 0, 0, 3, 1", "c2": "k_gather<16, 0, 0, 0, 3, 1",
-                 "c3": "k_gather_pick<16, 4>", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
+                 "c3": "k_gather_pick<16, 4", "c4": "k_gather<16, 1, 0, 0, 16, 4"}
 GATHER_LABEL = {"c1": "k_gather (fused argmax)", "c2": "k_gather (fused argmax)",
                 "c3": "k_gather_pick (gather with the top-K prune test in its loop, no maps)",
                 "c4": "k_gather (K = 3, fused argmax)"}

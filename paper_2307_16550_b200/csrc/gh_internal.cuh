@@ -175,6 +175,56 @@ __host__ __device__ __forceinline__ void tile_local(const TileDesc& td, int64_t 
   }
 }
 
+// Lane-ordered, bank-complementary entry order of a full-ring plan with
+// P <= 3 pairs (permute_for_banks, gh_table.cu). `uniq` are the plan's bins
+// in increasing order, par[i] the parity vector of uniq[i]'s ring rows (bit p
+// = row parity of pair p). At most 4 complementary couples (v, ~v) exist and
+// the gather's 8 lane groups (entry mod 8) form 4 entry pairs: pair class j
+// takes its couple's bins in increasing order (entries 8m + 2j, 8m + 2j + 1 =
+// the couple's next bin of class v and of class ~v). Every entry pair is
+// then bank-complementary and every lane group meets its bins in increasing
+// order, so the gather's "first strict maximum" per lane is the smallest bin
+// on an exact tie. The bins left when the shortest couple runs out follow in
+// ascending order. Appends to *order; returns the first entry of that tail
+// (a multiple of 32: the ordered part ends on a gather block).
+inline int64_t order_lane_monotone(const std::vector<uint32_t>& uniq,
+                                   const std::vector<unsigned>& par, int P,
+                                   std::vector<uint32_t>* order) {
+  const unsigned full = (1u << P) - 1u;
+  std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
+  for (size_t u = 0; u < uniq.size(); ++u) bucket[par[u] & full].push_back(uniq[u]);
+  const int ncpl = 1 << (P - 1), per = 4 / ncpl;
+  int64_t steps = INT64_MAX;
+  for (int c = 0; c < ncpl; ++c) {
+    const size_t n = bucket[c].size() < bucket[full ^ c].size() ? bucket[c].size()
+                                                                 : bucket[full ^ c].size();
+    const int64_t s = static_cast<int64_t>(n) / per;
+    steps = s < steps ? s : steps;
+  }
+  steps -= steps % 4;
+  const size_t base = order->size();
+  for (int64_t m = 0; m < steps; ++m)
+    for (int j = 0; j < 4; ++j) {
+      const int c = j / per;
+      const size_t i = static_cast<size_t>(m * per + j % per);
+      order->push_back(bucket[c][i]);
+      order->push_back(bucket[full ^ c][i]);
+    }
+  const int64_t tie_from = static_cast<int64_t>(order->size() - base);
+  std::vector<uint32_t> rest;
+  for (auto& b : bucket)
+    for (size_t i = static_cast<size_t>(steps * per); i < b.size(); ++i) rest.push_back(b[i]);
+  // ascending (insertion into a sorted run keeps the header free of <algorithm>)
+  for (size_t i = 1; i < rest.size(); ++i) {
+    const uint32_t x = rest[i];
+    size_t k = i;
+    for (; k > 0 && rest[k - 1] > x; --k) rest[k] = rest[k - 1];
+    rest[k] = x;
+  }
+  order->insert(order->end(), rest.begin(), rest.end());
+  return tie_from;
+}
+
 struct Plan {
   bool built = false;
   bool full = false;

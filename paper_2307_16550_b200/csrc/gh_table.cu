@@ -456,36 +456,12 @@ void permute_for_banks(Ctx* ctx, Table* t, Plan& pl) {
   };
   std::vector<std::vector<uint32_t>> bucket(static_cast<size_t>(full) + 1);
   if (P <= 3) {
-    // Ordered plan. At most 4 complementary couples (v, ~v) and the gather's
-    // 8 lane groups (entry mod 8) form 4 entry pairs: pair class j takes its
-    // couple's bins in increasing order (entries 8m + 2j, 8m + 2j + 1 = the
-    // couple's next bin of class v and of class ~v). Every entry pair is
-    // bank-complementary, and every lane group meets its bins in increasing
-    // order — so the gather's "first strict maximum" per lane is the
-    // smallest bin on exact ties, with nothing extra in its loop. The bins
-    // left when the shortest couple runs out (class counts differ by a few
-    // per cent) follow in ascending order; from there on (tie_from) the
-    // gather compares bins on exact ties.
-    for (int64_t u = 0; u < nu; ++u) bucket[parity(uniq[static_cast<size_t>(u)])].push_back(uniq[static_cast<size_t>(u)]);
-    const int ncpl = 1 << (P - 1), per = 4 / ncpl;
-    int64_t steps = INT64_MAX;
-    for (int c = 0; c < ncpl; ++c)
-      steps = std::min<int64_t>(
-          steps, static_cast<int64_t>(std::min(bucket[c].size(), bucket[full ^ c].size())) / per);
-    steps -= steps % 4;  // the ordered part ends on a 32-entry block
-    for (int64_t m = 0; m < steps; ++m)
-      for (int j = 0; j < 4; ++j) {
-        const int c = j / per;
-        const size_t i = static_cast<size_t>(m * per + j % per);
-        order.push_back(bucket[c][i]);
-        order.push_back(bucket[full ^ c][i]);
-      }
-    std::vector<uint32_t> rest;
-    for (auto& b : bucket)
-      for (size_t i = static_cast<size_t>(steps * per); i < b.size(); ++i) rest.push_back(b[i]);
-    std::sort(rest.begin(), rest.end());
-    pl.tie_from = static_cast<int64_t>(order.size());
-    order.insert(order.end(), rest.begin(), rest.end());
+    // Ordered plan (order_lane_monotone, gh_internal.cuh): every entry pair
+    // bank-complementary, every lane group's bins in increasing order, the
+    // unmatched bins as an ascending tail from tie_from on.
+    std::vector<unsigned> par(static_cast<size_t>(nu));
+    for (int64_t u = 0; u < nu; ++u) par[static_cast<size_t>(u)] = parity(uniq[static_cast<size_t>(u)]);
+    pl.tie_from = order_lane_monotone(uniq, par, P, &order);
   } else {
     // more couples than entry pairs: greedy matching of v with ~v inside
     // windows of 1024 bins; no lane order, so the gather compares bins on
