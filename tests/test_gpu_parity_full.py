@@ -160,3 +160,37 @@ def test_c3_top5_assignment_statistics(ctx):
     assert cell["estimates"] == sc.topk * T
     assert_cell_equals(cell, ref_stats)
     assert (assign >= -1).all()
+
+
+def test_c3_full_grid_pick_engine_at_scale(ctx):
+    # BASELINE c3 at the bench's shape: one 8-trial batch per SM and more on
+    # the whole 10^6-bin grid, so `auto` runs the map-free pick engine
+    # (k_gather_pick) the way the bench does. Its lists must be exactly the
+    # map-then-pick engine's (the same fp32 sums), on the plain and on the
+    # bounds-tested build, and match the oracle rule on a sample of trials.
+    sc = S.baseline("c3")
+    T, k = 8 * 148 * 2 + 3, sc.topk
+    t = gh.precompute_hop_table(ctx, sc)
+    fr, _ = gh.synthesize(ctx, sc, 0, T)
+    ctx.set_topk_impl("auto")
+    ai, av = gh.hop_topk(ctx, t, fr, k)
+    ctx.set_topk_impl("map")
+    try:
+        mi, mv = gh.hop_topk(ctx, t, fr, k)
+    finally:
+        ctx.set_topk_impl("auto")
+    assert np.array_equal(ai.cpu().numpy(), mi.cpu().numpy())
+    assert np.array_equal(av.cpu().numpy(), mv.cpu().numpy())
+    ctx.set_debug_checks(True)
+    try:
+        ci, cv = gh.hop_topk(ctx, t, fr, k)
+    finally:
+        ctx.set_debug_checks(False)
+    assert np.array_equal(ci.cpu().numpy(), ai.cpu().numpy())
+    assert np.array_equal(cv.cpu().numpy(), av.cpu().numpy())
+    # the oracle on a few of those trials (device-synthesised frames, fp64 maps)
+    sub = np.array([0, 7, 1184, T - 1])
+    oi, oc, _ = O.build_table(sc)
+    frs = fr[torch.from_numpy(sub).cuda()].cpu().numpy().astype(np.complex128)
+    ref = hop_maps(O.spectra(frs, sc.n_fft), oi, oc)
+    topk_parity(ref, ai.cpu().numpy()[sub], sc, k, "c3 pick engine at scale")
