@@ -182,3 +182,27 @@ def test_pick_engine_bounds_checked_build(ctx, fused_engine):
         assert np.array_equal(ci.cpu().numpy(), pi.cpu().numpy())
         assert np.array_equal(cv.cpu().numpy(), pv.cpu().numpy())
         assert (zi.cpu().numpy()[:, 0] == 0).all()
+
+
+def test_argmax_through_the_pick_engine(ctx, fused_engine):
+    # hop_argmax with at least one 8-trial batch per SM on a tiled K = 1 plan
+    # runs the pick engine's K = 1 form: the same bins and values as the
+    # plain fused-argmax gather (small batches) and as the maps' first maximum
+    if fused_engine != "pick":
+        pytest.skip("engine-independent")
+    ctx.set_topk_impl("auto")
+    sc = c3_sub(96, 82)
+    T = 8 * 148 + 5
+    t = gh.precompute_hop_table(ctx, sc)
+    fr, _ = gh.synthesize(ctx, sc, 0, T)
+    bi, bv = gh.hop_argmax(ctx, t, fr)                       # routed: 149 batches
+    parts = [gh.hop_argmax(ctx, t, fr[a:a + 512]) for a in range(0, T, 512)]  # plain gather
+    pi = torch.cat([p[0] for p in parts])
+    pv = torch.cat([p[1] for p in parts])
+    assert np.array_equal(bi.cpu().numpy(), pi.cpu().numpy())
+    assert np.array_equal(bv.cpu().numpy(), pv.cpu().numpy())
+    m = gh.hop_decision_map(ctx, t, fr[:64]).cpu().numpy()
+    assert np.array_equal(bi.cpu().numpy()[:64], m.argmax(axis=1))
+    # zero frames: the plateau's first bin
+    zi, zv = gh.hop_argmax(ctx, t, torch.zeros_like(fr))
+    assert (zi.cpu().numpy() == 0).all() and (zv.cpu().numpy() == 0).all()
