@@ -218,9 +218,11 @@ void check_synth_flag(gh::Ctx* c, const gh::SynthParams& sp) {
   if (h & 1) fail(GH_ERUNTIME, "scene outside unambiguous window");
 }
 
-// Top-K local maxima per trial (BASELINE c3): maps of a trial chunk are
-// materialised (<= 8 GiB of the 180 GB HBM: ~2000 c3 trials, so the FFT and
-// gather launches fill the GPU), then k_topk_localmax picks the peaks.
+// Top-K local maxima per trial (BASELINE c3) through one of three engines
+// (below); every engine returns the same lists. The map engine materialises
+// the maps of a trial chunk (<= 8 GiB of the 180 GB HBM: ~2000 c3 trials, so
+// the FFT and gather launches fill the GPU), then k_topk_localmax picks the
+// peaks.
 void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp, int T,
               int combine, int K, int64_t* idx_d, float* val_d) {
   // Engines (gh_ctx_set_topk_impl): 3 = the gather with the prune test in its
