@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgridhop_b200.so"
-SOURCES = ["gh_api.cu", "gh_fft.cu", "gh_table.cu", "gh_gather.cu", "gh_gather_topk.cu", "gh_gather_pick.cu", "gh_direct.cu",
+SOURCES = ["gh_api.cu", "gh_fft.cu", "gh_table.cu", "gh_gather.cu", "gh_gather_k3.cu", "gh_gather_topk.cu", "gh_gather_pick.cu", "gh_direct.cu",
            "gh_direct_umma.cu", "gh_peaks.cu", "gh_topk.cu", "gh_indirect.cu",
            "gh_velocity.cu", "gh_campaign.cu"]
 

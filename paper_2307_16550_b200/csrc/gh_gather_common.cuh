@@ -1,4 +1,4 @@
-// gh_gather_common.cuh — pieces shared by the gather kernels (gh_gather.cu)
+// gh_gather_common.cuh — pieces shared by the gather kernels (gh_gather_impl.cuh)
 // and the fused top-K gather (gh_gather_topk.cu): the launch arguments and
 // the per-pair accumulate step.
 #pragma once

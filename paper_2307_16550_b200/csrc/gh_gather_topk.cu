@@ -1,5 +1,5 @@
 // gh_gather_topk.cu — BASELINE c3's fused gather + top-K local-maximum
-// pick (sm_100a). The gather is the one of gh_gather.cu (hopping.cpp:59-117
+// pick (sm_100a). The gather is the one of gh_gather_impl.cuh (hopping.cpp:59-117
 // hop_bin_value with Mc = 1); the pick is the rule of or_topk_local_max /
 // k_topk_localmax (ties to the smallest bin, direct.cpp:55-62).
 #include <cuda_runtime.h>

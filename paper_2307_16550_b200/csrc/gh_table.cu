@@ -858,7 +858,7 @@ Plan& build_plan(Ctx* ctx, Table* t, bool mapmode) {
 // batches as the argmax plan, but each tile's core box is grown by a 1-bin
 // halo so the gather itself evaluates every neighbour a core bin's
 // local-maximum test needs; the tile's values for its 8 trials then stay in
-// shared memory next to the range windows (gh_gather.cu k_gather_topk).
+// shared memory next to the range windows (gh_gather_topk.cu k_gather_topk).
 // Windows + values must share one CTA's shared memory, so tiles are smaller
 // than the argmax plan's (~56 x 56 bins on c3 instead of ~113 x 113).
 constexpr size_t kTopkSmem = 224 * 1024;  // windows + values + lists, per SM
