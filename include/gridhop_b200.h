@@ -113,8 +113,8 @@ int gh_ctx_reset_timing(gh_ctx* ctx);
 int gh_ctx_set_direct_impl(gh_ctx* ctx, int32_t impl);
 /* Top-K local-maximum engine (BASELINE c3): 0 = auto (engine 3 where the
  * table's plan admits it — tiled K = 1 plans of at most 16 pairs — and the
- * call has at least one 8-trial batch per SM, else engine 2); 1 = halo tiles
- * with the tile's values in shared memory; 2 = map-mode gather, then
+ * call's 8-trial batches fill its rounds of one batch per SM, else engine 2);
+ * 1 = halo tiles with the tile's values in shared memory; 2 = map-mode gather, then
  * k_topk_localmax over the maps in HBM; 3 = the gather with the prune test in
  * its loop and candidates verified against the table and spectra (no maps).
  * All engines return identical bins and values. */

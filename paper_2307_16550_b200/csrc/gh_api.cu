@@ -129,6 +129,16 @@ void check_combine(int combine) {
 }
 
 // spectra in the gather layout for table t, from frames or from synthesis
+// The pick engine hands 8-trial batches to one CTA per SM: its last round is
+// only partly filled, so it pays when batches / (rounds * SMs) times its
+// measured per-trial advantage over the alternative (c3: 1.5x over map then
+// pick, 1.1x over the fused-argmax gather) reaches 1.
+bool pick_pays(const gh::Ctx* c, int n_batches, double advantage) {
+  if (n_batches < c->num_sms) return false;
+  const int rounds = (n_batches + c->num_sms - 1) / c->num_sms;
+  return advantage * n_batches >= static_cast<double>(rounds) * c->num_sms;
+}
+
 void* gather_spectra(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthParams* sp,
                      int T, int combine, bool mapmode) {
   const gh::Plan& pl = gh::build_plan(c, t, mapmode);
@@ -153,7 +163,7 @@ void hop_argmax(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthP
     // the plain gather: their argmax covers the halo layers too.
     const gh::Plan& ap = t->plan;
     if (c->topk_impl == 0 && gh::gather_pick_ok(t, ap, 1) && t->core_hi <= t->core_lo &&
-        (T + ap.tb - 1) / ap.tb >= c->num_sms) {
+        pick_pays(c, (T + ap.tb - 1) / ap.tb, 1.1)) {
       gh::launch_gather_pick(c, t, spec, T, 1, idx_d, val_d);
       return;
     }
@@ -228,14 +238,14 @@ void hop_topk(gh::Ctx* c, gh::Table* t, const float2* frames, const gh::SynthPar
   // Engines (gh_ctx_set_topk_impl): 3 = the gather with the prune test in its
   // loop (gh_gather_pick.cu), 1 = halo tiles with values in shared memory
   // (gh_gather_topk.cu), 2 = map then pick. auto (0) takes engine 3 where the
-  // plan admits it and there is a batch per SM to hand out, else 2; every
-  // engine returns the same lists.
+  // plan admits it and its rounds of one batch per SM are full enough to pay
+  // (pick_pays), else 2; every engine returns the same lists.
   if (c->topk_impl == 0 || c->topk_impl == 3) {
     const gh::Plan& ap = gh::build_plan(c, t, false);
     const bool ok = gh::gather_pick_ok(t, ap, K);
     if (c->topk_impl == 3 && !ok)
       fail(GH_EINVAL, "top-k: the pick engine needs a tiled K = 1 plan of at most 16 pairs");
-    if (ok && (c->topk_impl == 3 || (T + ap.tb - 1) / ap.tb >= c->num_sms)) {
+    if (ok && (c->topk_impl == 3 || pick_pays(c, (T + ap.tb - 1) / ap.tb, 1.5))) {
       // trial chunks bound the spectra scratch (~16 GiB of the 180 GB) and
       // split T evenly, so every launch hands each SM many batches
       const int tb = ap.tb;

@@ -152,7 +152,7 @@ def test_auto_engine_takes_pick_on_large_batches(ctx, fused_engine):
     if fused_engine != "pick":
         pytest.skip("engine-independent")
     sc = c3_sub(96, 82)
-    T, k = 8 * 148 + 5, 5
+    T, k = 8 * 148 * 2 - 3, 5  # two full rounds of one batch per SM, the last batch ragged
     t = gh.precompute_hop_table(ctx, sc)
     ctx.set_topk_impl("auto")
     ai, av = gh.campaign_hop_topk(ctx, t, sc, 0, T, k)
@@ -192,10 +192,10 @@ def test_argmax_through_the_pick_engine(ctx, fused_engine):
         pytest.skip("engine-independent")
     ctx.set_topk_impl("auto")
     sc = c3_sub(96, 82)
-    T = 8 * 148 + 5
+    T = 8 * 148 * 2 - 3  # two full rounds of one batch per SM, the last batch ragged
     t = gh.precompute_hop_table(ctx, sc)
     fr, _ = gh.synthesize(ctx, sc, 0, T)
-    bi, bv = gh.hop_argmax(ctx, t, fr)                       # routed: 149 batches
+    bi, bv = gh.hop_argmax(ctx, t, fr)                       # routed: 296 batches
     parts = [gh.hop_argmax(ctx, t, fr[a:a + 512]) for a in range(0, T, 512)]  # plain gather
     pi = torch.cat([p[0] for p in parts])
     pv = torch.cat([p[1] for p in parts])
