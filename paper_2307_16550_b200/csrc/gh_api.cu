@@ -427,10 +427,15 @@ void host_frames_pipeline(gh::Ctx* c, gh::Table* t, const double* frames, int n_
                           int64_t* idx, double* val, Run&& run) {
   const int64_t per = (int64_t)t->P * t->N;
   // ~32 chunks (>= 256 trials each): the copies stream back to back and only
-  // the last chunk's compute is exposed (1/32 of the step; measured 8 chunks:
-  // e2e 528 ms vs the 472 ms PCIe bound on c3)
+  // the first copy and the last chunk's compute are exposed (measured 8
+  // chunks: e2e 528 ms vs the 472 ms PCIe bound on c3; 31 chunks: 486 ms)
   int chunk = n_trials;
   if (n_trials >= 2048) chunk = std::max(256, ((n_trials + 31) / 32 + 255) / 256 * 256);
+  // large calls: chunks of whole rounds of one 8-trial batch per SM (what the
+  // pick engine hands out), ~80 of them: the exposed first copy and last
+  // compute shrink with the chunk (c3: 3,328 -> 1,184 trials per chunk)
+  const int unit = 8 * c->num_sms;
+  if (chunk > unit) chunk = unit * std::max(1, (n_trials / 80 + unit / 2) / unit);
   const int n_chunks = (n_trials + chunk - 1) / chunk;
   const size_t b128 = sizeof(double2) * per * chunk;
   const int64_t nres = (int64_t)n_trials * k;
